@@ -1,0 +1,213 @@
+/* skrull.h -- C ABI of libskrull.so: the B200-native hot path of Skrull (arXiv 2505.19609).
+ *
+ * Citations: P:n = line n of PAPER.md (the paper's LaTeX), S:n = line n of SPEC.md,
+ * R# = a reading in DESIGN.md's ambiguity ledger.
+ *
+ * Conventions (all entry points)
+ *  - Every function returning skr_status never throws, aborts or exits. On failure it returns a
+ *    non-zero status and skr_last_error() holds a thread-local message.
+ *  - The caller allocates ALL outputs (host and device) and owns them; sizes come from the
+ *    *_bounds / *_ws_bytes queries. The library keeps no pointer past the call, except inside
+ *    explicit opaque objects (skr_comm) with create/destroy pairs.
+ *  - Host functions are pure and re-entrant. Device functions enqueue work on the caller's
+ *    stream(s) and return without synchronising; errors of the enqueued work surface at the
+ *    caller's next synchronisation (launch errors are returned as SKR_E_CUDA immediately).
+ *  - Device entry points require an sm_100a GPU (B200); on anything else they return
+ *    SKR_E_UNSUPPORTED. There is no CPU fallback.
+ *  - Integers: sequence lengths int64; row indices and table entries int32 (a packed rank
+ *    buffer holds < 2^31 rows).
+ */
+#ifndef SKRULL_H_
+#define SKRULL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t skr_status;
+enum {
+  SKR_OK = 0,
+  SKR_E_ARG = 1,         /* bad argument (null pointer, negative size, inconsistent shape) */
+  SKR_E_SCHEDULE = 2,    /* Alg. 1 Assert: roll-back impossible, or disabled (Table 3 "OOM") */
+  SKR_E_GDS = 3,         /* Alg. 2: no init <= |Subset|+1 feasible (R15) */
+  SKR_E_BUDGET = 4,      /* Memory(S) budget <= beta (Appendix C.1) */
+  SKR_E_PROFILE = 5,     /* fewer than 2 profile points at/above the threshold */
+  SKR_E_OVERFLOW = 6,    /* exact integer FLOPs / scaled ledgers would overflow int64 */
+  SKR_E_CAPACITY = 7,    /* caller buffer too small */
+  SKR_E_CUDA = 8,        /* CUDA launch / runtime error */
+  SKR_E_NCCL = 9,        /* NCCL error */
+  SKR_E_UNSUPPORTED = 10 /* no sm_100a device, or shape outside the kernels' support */
+};
+
+const char* skr_status_string(skr_status s);
+const char* skr_last_error(void);
+int32_t skr_abi_version(void); /* bumps on any signature change */
+
+/* ------------------------------------------------------------------ a1: cost model
+ * Appendix C. */
+typedef struct {
+  int64_t hidden;     /* h   = Hq * d */
+  int64_t kv_hidden;  /* h_kv = Hkv * d */
+  int64_t pack_batch; /* b, 1 with sequence packing */
+} skr_model;
+typedef struct {
+  double slope;     /* alpha */
+  double intercept; /* beta / T_fixed */
+} skr_fit;
+typedef struct {
+  skr_fit comp;          /* Eq. 13: T_comp = alpha FLOPs + beta */
+  skr_fit comm;          /* Eq. 15: T_comm = alpha V + T_fixed, 0 when V == 0    (R26) */
+  skr_fit mem;           /* Memory(S) = alpha S + beta */
+  double bytes_per_elem; /* V is Eq. 14 elements x bytes_per_elem              (R25) */
+  double dist_penalty;   /* multiplies T_comp(Dist); 1 = Eq. 2 exactly  */
+} skr_cost;
+typedef struct {
+  int32_t cp;            /* N, CP degree */
+  int32_t dp;            /* ws, DP degree */
+  int64_t bucket_tokens; /* C, BucketSize per rank */
+  int32_t rollback;      /* 1 = Alg. 3 RollBack enabled; 0 reproduces Table 3's "w/o" rows */
+} skr_cluster;
+
+/* Eq. 12: FLOPs(S) = 20 b h^2 S + 4 b h h_kv S + 4 b h S^2, exact. SKR_E_OVERFLOW past int64. */
+skr_status skr_flops(int64_t S, const skr_model* m, int64_t* out);
+/* Eq. 14: Volume(S) = b S h_kv elements. */
+skr_status skr_volume(int64_t S, const skr_model* m, int64_t* out);
+/* Eq. 13; zero FLOPs cost zero (R36). */
+double skr_t_comp(double flops, const skr_fit* fit);
+/* Eq. 15; 0 when volume == 0 (R26). */
+double skr_t_comm(double volume, const skr_fit* fit);
+/* Least squares over points with x >= min_x; negative intercept clamped to 0.
+ * SKR_E_PROFILE with < 2 qualifying points. */
+skr_status skr_fit_linear(const double* x, const double* y, int32_t n, double min_x, skr_fit* out);
+/* C = floor((budget - beta) / alpha); SKR_E_BUDGET if budget <= beta. */
+skr_status skr_bucket_size(double budget, const skr_fit* mem, int64_t* C);
+
+/* ------------------------------------------------------------------ a2/a3: schedulers */
+/* Alg. 1 + Alg. 3 (readings R1-R10). `lens[K]` in input order; writes
+ * assign[K] in input order: -1 = distributed, v in [0,cp) = local on CP rank v.
+ * Exact integer ledgers scaled by N (R4). On SKR_E_SCHEDULE, *fail_idx = sorted position of the
+ * sequence that could not be placed. n_rollbacks / fail_idx may be NULL. */
+skr_status skr_dacp(const int64_t* lens, int32_t K, const skr_cluster* cl, const skr_model* m, int32_t* assign,
+                    int32_t* n_rollbacks, int32_t* fail_idx);
+/* Eq. 1-7 for a given assignment. per_rank_time[cp] (may be NULL); an infeasible
+ * plan (Eq. 7) is still evaluated with *feasible = 0. */
+skr_status skr_eval_tdacp(const int64_t* lens, const int32_t* assign, int32_t K, const skr_cluster* cl,
+                          const skr_model* m, const skr_cost* cost, double* per_rank_time, double* comm_time,
+                          double* dist_time, double* tdacp, int32_t* feasible);
+/* Alg. 2 line 1 "Binpack(ws, FLOPs(S[K]))" as greedy LPT (R16). bin_of_seq[K]. */
+skr_status skr_lpt(const int64_t* lens, int32_t K, int32_t bins, const skr_model* m, int32_t* bin_of_seq);
+/* Alg. 2 (R11-R15) for DP rank `dp_rank`: mb_of_seq[K] = micro-batch index of each
+ * sequence of this rank's LPT bin, -1 for sequences of other DP ranks. */
+skr_status skr_gds(const int64_t* lens, int32_t K, const skr_cluster* cl, const skr_model* m, int32_t dp_rank,
+                   int32_t* mb_of_seq, int32_t* n_mb);
+/* Whole-iteration plan: LPT over cl->dp ranks, GDS per rank, DACP per micro-batch.
+ * dp_of_seq[K], mb_of_seq[K], assign[K] (DACP result inside its micro-batch), n_mb_per_dp[cl->dp].
+ * Every rank computes the identical plan with no communication. */
+skr_status skr_plan(const int64_t* lens, int32_t K, const skr_cluster* cl, const skr_model* m, int32_t* dp_of_seq,
+                    int32_t* mb_of_seq, int32_t* assign, int32_t* n_mb_per_dp, int32_t* n_rollbacks);
+
+/* ------------------------------------------------------------------ a4: packer (host)
+ * One micro-batch (mb_lens[K_mb] in micro-batch input order, its DACP assign), CP rank `rank`.
+ * Layout (R20-R23): zigzag chunks c of 2N, [floor(cS/2N), floor((c+1)S/2N)), rank j owns j and
+ * 2N-1-j; packed rows = [distributed chunks, sequences ascending (length, index), chunk j then
+ * 2N-1-j] ++ [locals on j, ascending]. Source order ("rank-natural"): this rank's rows in input
+ * order, positions ascending. */
+skr_status skr_pack_bounds(const int64_t* mb_lens, const int32_t* assign, int32_t K_mb, int32_t cp, int32_t rank,
+                           int32_t* n_seg, int32_t* n_dist_seg, int32_t* n_rows, int32_t* dist_rows,
+                           int32_t* pad_rows_P, int32_t* natural_rows, int32_t* n_chunks);
+/* Writes cu_seqlens_q[n_seg+1], q_pos/k_start/k_len/seg_seq/seg_chunk[n_seg], src_row[n_rows].
+ * k_start: packed row of the segment (locals) or row in the natural distributed-K/V buffer
+ * (distributed). k_len = q_pos + q_len (bottom-right causal). */
+skr_status skr_pack_rank(const int64_t* mb_lens, const int32_t* assign, int32_t K_mb, int32_t cp, int32_t rank,
+                         int32_t* cu_seqlens_q, int32_t* q_pos, int32_t* k_start, int32_t* k_len, int32_t* seg_seq,
+                         int32_t* seg_chunk, int32_t* src_row);
+/* Chunk table of all distributed sequences (the same on every rank): n_chunks rows of 6 int32:
+ * {seq, chunk, owner, gathered_row (owner*P + offset in owner's prefix), natural_row, len}. */
+skr_status skr_pack_chunks(const int64_t* mb_lens, const int32_t* assign, int32_t K_mb, int32_t cp,
+                           int32_t* chunk_table);
+/* Attention work lists (host): pairs {segment, tile} ordered longest-work-first (LPT).
+ * fwd: query tiles of block_m rows; bwd: key tiles of block_n rows over [0, k_len). */
+skr_status skr_tiles_fwd(const int32_t* cu_seqlens_q, const int32_t* q_pos, int32_t n_seg, int32_t block_m,
+                         int32_t* tiles, int32_t cap_tiles, int32_t* n_tiles);
+skr_status skr_tiles_bwd(const int32_t* cu_seqlens_q, const int32_t* q_pos, const int32_t* k_len, int32_t n_seg,
+                         int32_t block_n, int32_t* tiles, int32_t cap_tiles, int32_t* n_tiles);
+
+/* ------------------------------------------------------------------ a5-a9: device
+ * All pointers below are DEVICE pointers; `stream` is a cudaStream_t passed as void*. */
+enum { SKR_BF16 = 0, SKR_FP32 = 1 };
+typedef struct {
+  int32_t hq, hkv, d; /* q heads, kv heads (hq % hkv == 0, GQA groups contiguous, R30), head dim */
+  int32_t dtype;      /* SKR_BF16: tcgen05 kernels (d in {64,128}); SKR_FP32: fp32 test mode (R31) */
+  float scale;        /* softmax scale, 1/sqrt(d) (R29) */
+} skr_attn_shape;
+typedef struct {                /* one segment class (locals, or distributed chunks) of one rank */
+  const int32_t* cu_seqlens_q;  /* [n_seg+1] packed query rows */
+  const int32_t* q_pos;         /* [n_seg] position of the first query in its sequence */
+  const int32_t* k_start;       /* [n_seg] first row of the segment's keys in the K/V buffer */
+  const int32_t* k_len;         /* [n_seg] number of keys = q_pos + q_len */
+  const int32_t* tiles;         /* [2*n_tiles] work list from skr_tiles_fwd / skr_tiles_bwd */
+  int32_t n_seg, n_tiles;
+  int32_t row_begin, row_end;   /* host ints: the class's packed query rows are [row_begin, row_end) */
+} skr_segs;
+
+/* Forward (row a7; Eq. 2-4): per segment and q-head h (kv head h*hkv/hq),
+ * O = softmax(scale QK^T + bottom-right causal mask) V, LSE = natural-log row logsumexp.
+ * q, o: [n_q_rows][hq][d]; k, v: [n_kv_rows][hkv][d]; lse: fp32 [hq][n_q_rows].
+ * bf16 in/out with fp32 accumulation (SKR_BF16) or fp32 throughout (SKR_FP32).
+ * `tiles` must come from skr_tiles_fwd with block_m = skr_attn_block_m(shape). */
+int32_t skr_attn_block_m(const skr_attn_shape* s);
+int32_t skr_attn_block_n(const skr_attn_shape* s);
+skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k, const void* v,
+                        void* o, float* lse, int32_t n_q_rows, int32_t n_kv_rows, void* stream);
+/* Backward (row a8): D = rowsum(dO o O); dQ, dK, dV of the plain definition.
+ * dq: [n_q_rows][hq][d] written for the segments' rows (bf16 / fp32 per dtype).
+ * kv_accumulate = 0: dk, dv [n_kv_rows][hkv][d] of dtype are WRITTEN for the segments' key rows
+ *   (locals: each key row belongs to exactly one segment).
+ * kv_accumulate = 1: dk, dv are fp32 [n_kv_rows][hkv][d] and are ADDED to (distributed chunks of one
+ *   sequence share key rows; the caller zeroes them once).
+ * ws: fp32 scratch of skr_attn_bwd_ws_bytes(). `tiles` from skr_tiles_bwd, block_n = skr_attn_block_n. */
+size_t skr_attn_bwd_ws_bytes(const skr_attn_shape* s, int32_t n_q_rows);
+skr_status skr_attn_bwd(const skr_attn_shape* s, const skr_segs* g, const void* q,
+                        const void* k, const void* v, const void* o, const void* dout, const float* lse, void* dq,
+                        void* dk, void* dv, int32_t kv_accumulate, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* a5 pack: dst[r] = src[src_row[r]] for n_rows rows of row_bytes (multiple of 16). */
+skr_status skr_pack_rows(const void* src, const int32_t* src_row, int32_t n_rows, int32_t row_bytes, void* dst,
+                         void* stream);
+/* a5 inverse: dst[src_row[r]] = src[r]. */
+skr_status skr_unpack_rows(const void* src, const int32_t* src_row, int32_t n_rows, int32_t row_bytes, void* dst,
+                           void* stream);
+/* a6 reorder: gathered [N][P] rank-major rows -> natural distributed order, via the chunk table. */
+skr_status skr_gather_chunks(const void* gathered, const int32_t* chunk_table, int32_t n_chunks, int32_t row_bytes,
+                             void* natural, void* stream);
+/* a9 permute: natural fp32 partials -> rank-major [N][P] rows (rows beyond a rank's count zeroed). */
+skr_status skr_scatter_chunks(const void* natural, const int32_t* chunk_table, int32_t n_chunks, int32_t row_bytes,
+                              int32_t pad_rows_P, int32_t cp, void* rankmajor, void* stream);
+/* a9 cast: fp32 -> bf16, n elements. */
+skr_status skr_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* CP communicator (rows a6/a9; NCCL inside the CP group over NVLink/NVSwitch). */
+typedef struct skr_comm skr_comm;
+int32_t skr_nccl_id_bytes(void); /* size of the unique id blob (128) */
+skr_status skr_nccl_get_id(void* id_out);
+skr_status skr_comm_create(const void* nccl_id, int32_t nranks, int32_t rank, skr_comm** out);
+void skr_comm_destroy(skr_comm* c);
+skr_status skr_comm_all_gather(skr_comm* c, const void* send, void* recv, size_t bytes_per_rank, void* stream);
+skr_status skr_comm_reduce_scatter_f32(skr_comm* c, const float* send, float* recv, size_t count_per_rank,
+                                       void* stream);
+skr_status skr_comm_all_reduce_f32(skr_comm* c, float* buf, size_t count, void* stream);
+
+/* ------------------------------------------------------------------ diagnostics */
+/* UMMA/TMA/TMEM building-block self-test: C[128][n] fp32 from bf16 A/B with operand layout
+ * `variant` (0: A K-major, B K-major; 1: B MN-major; 2: A and B MN-major; 3: A written by threads
+ * into swizzled smem). n in {64,128}, K = 128. */
+skr_status skr_selftest_umma(int32_t variant, int32_t n, const void* A, const void* B, float* C, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKRULL_H_ */

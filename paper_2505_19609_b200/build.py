@@ -1,0 +1,118 @@
+"""Build libskrull.so in-tree: nvcc for sm_100a (CUDA sources) + g++ (host planner).
+
+    python -m paper_2505_19609_b200.build [--clean] [-j N]
+
+Objects go to build/ at the repo root; the shared library lands next to this file so it
+travels with gpurun snapshots. Incremental on source / header mtimes.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(ROOT, "build")
+LIB = os.path.join(PKG, "libskrull.so")
+INCLUDE = os.path.join(ROOT, "include")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    try:
+        import nvidia.nccl  # noqa: F401
+        base = os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+        if os.path.exists(os.path.join(base, "include", "nccl.h")):
+            return base
+    except Exception:
+        pass
+    return None
+
+
+def _flags():
+    nccl = _nccl_dir()
+    inc = ["-I", INCLUDE, "-I", CSRC]
+    if nccl:
+        inc += ["-I", os.path.join(nccl, "include")]
+    cu = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+          "--expt-relaxed-constexpr", "-Xptxas", "-v", *inc]
+    cc = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
+          "-Wno-unused-parameter", "-I", os.path.join(CUDA, "include"), *inc]
+    link = [NVCC, *ARCH, "-shared", "-o", LIB, "-Xlinker", "--no-undefined"]
+    libs = ["-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    if nccl:
+        libs += ["-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+                 "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
+    return cu, cc, link, libs, nccl is not None
+
+
+def _sources():
+    cus = sorted(glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True))
+    ccs = sorted(glob.glob(os.path.join(CSRC, "**", "*.cc"), recursive=True))
+    hdrs = sorted(glob.glob(os.path.join(CSRC, "**", "*.h"), recursive=True)
+                  + glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True)
+                  + glob.glob(os.path.join(INCLUDE, "*.h")))
+    return cus, ccs, hdrs
+
+
+def build(jobs: int = 8, verbose: bool = False, clean: bool = False) -> str:
+    if clean and os.path.isdir(BUILD):
+        shutil.rmtree(BUILD)
+    os.makedirs(BUILD, exist_ok=True)
+    cu_flags, cc_flags, link, libs, have_nccl = _flags()
+    if not have_nccl:
+        raise RuntimeError("nccl.h not found (pip nvidia-nccl); the CP collectives need it")
+    cus, ccs, hdrs = _sources()
+    hdr_mtime = max((os.path.getmtime(h) for h in hdrs), default=0)
+    jobs_list = []
+    objs = []
+    for src in cus + ccs:
+        rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
+        obj = os.path.join(BUILD, rel + ".o")
+        objs.append(obj)
+        if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
+            continue
+        flags = cu_flags if src.endswith(".cu") else cc_flags
+        jobs_list.append((src, flags + ["-c", src, "-o", obj], obj))
+
+    def run(job):
+        src, cmd, obj = job
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"compile failed: {src}\n{r.stderr}")
+        with open(obj + ".log", "w") as f:
+            f.write(r.stderr)
+        return src, r.stderr
+
+    with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
+        for src, err in ex.map(run, jobs_list):
+            if verbose:
+                print(f"[build] {os.path.relpath(src, ROOT)}")
+                if err.strip():
+                    print(err)
+    if jobs_list or not os.path.exists(LIB):
+        r = subprocess.run(link + objs + libs, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed\n{r.stderr}")
+    return LIB
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--clean", action="store_true")
+    ap.add_argument("-j", type=int, default=8)
+    ap.add_argument("-v", action="store_true")
+    a = ap.parse_args()
+    print(build(a.j, a.v, a.clean))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,114 @@
+// Building-block self-test: one 128 x n x 128 bf16 UMMA through each operand layout the
+// attention kernels use (TMA SW128 K-major, TMA SW128 MN-major, thread-written SW128 K-major).
+#include "device.cuh"
+#include "sm100.cuh"
+#include "tma.h"
+
+namespace skr {
+
+// smem: A 32 KB (two 64-wide chunks of 128 rows), B 32 KB, barriers.
+__global__ void __launch_bounds__(128, 1)
+    selftest_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                    const __nv_bfloat16* __restrict__ A, float* __restrict__ C, int variant, int n) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + 32768;
+  uint64_t* bar_tma = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint64_t* bar_mma = bar_tma + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_tma + 2);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_tma, 1);
+    mbar_init(bar_mma, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  // variant 3: A [128][128] written by threads into SW128 K-major smem (as P is in attention)
+  if (variant == 3) {
+    const int row = threadIdx.x;
+    for (int c = 0; c < 128; c += 8) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(A + row * 128 + c);
+      uint32_t base = smem_u32(sA + (c / 64) * 16384);
+      st_shared_v4(base + sw128_off(row, c % 64), src[0], src[1], src[2], src[3]);
+    }
+    fence_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (threadIdx.x == 0) {
+    const bool a_tma = variant != 3;
+    const bool b_mn = variant == 1 || variant == 2;
+    const bool a_mn = variant == 2;
+    uint32_t bytes = (a_tma ? 32768u : 0u) + (b_mn ? (uint32_t)n * 256u : (uint32_t)n * 256u);
+    mbar_expect_tx(bar_tma, bytes);
+    for (int ch = 0; ch < 2; ++ch) {
+      if (a_tma) tma_load_2d(sA + ch * 16384, &ta, bar_tma, ch * 64, 0);  // 64 cols x 128 rows
+    }
+    if (b_mn) {
+      // B global [K=128][n]: chunks of 64 n-columns x 128 K-rows
+      for (int ch = 0; ch < n / 64; ++ch) tma_load_2d(sB + ch * 16384, &tb, bar_tma, ch * 64, 0);
+    } else {
+      // B global [n][K=128]: chunks of 64 K-columns x n rows
+      for (int ch = 0; ch < 2; ++ch) tma_load_2d(sB + ch * (n * 128), &tb, bar_tma, ch * 64, 0);
+    }
+    mbar_wait(bar_tma, 0);
+    tc_fence_after();
+    const uint32_t idesc = idesc_bf16_f32(128, n, a_mn ? 1 : 0, b_mn ? 1 : 0);
+    for (int k = 0; k < 8; ++k) {
+      uint64_t ad, bd;
+      if (a_mn)
+        ad = sdesc_sw128(smem_u32(sA) + k * 2048, 16384, 1024);
+      else
+        ad = sdesc_sw128(smem_u32(sA) + (k / 4) * 16384 + (k % 4) * 32, 16, 1024);
+      if (b_mn)
+        bd = sdesc_sw128(smem_u32(sB) + k * 2048, 16384, 1024);
+      else
+        bd = sdesc_sw128(smem_u32(sB) + (k / 4) * (n * 128) + (k % 4) * 32, 16, 1024);
+      umma_f16(tmem, ad, bd, idesc, k > 0);
+    }
+    umma_commit(bar_mma);
+  }
+  __syncwarp();
+  mbar_wait(bar_mma, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 32; ++i) C[row * n + c0 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<128>(tmem);
+}
+
+}  // namespace skr
+
+SKR_EXPORT skr_status skr_selftest_umma(int32_t variant, int32_t n, const void* A, const void* B, float* C,
+                                         void* stream) {
+  using namespace skr;
+  if (skr_status s = check_sm100()) return s;
+  SKR_REQUIRE(variant >= 0 && variant <= 3 && (n == 64 || n == 128) && A && B && C, "bad selftest args");
+  CUtensorMap ta, tb;
+  const bool b_mn = variant == 1 || variant == 2;
+  // A: K-major [128][128] (variants 0,1) or MN-major given as [K=128][M=128] (variant 2): same shape.
+  if (!make_tmap_2d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 128, 128, 128, 128, 64, true))
+    return fail(SKR_E_CUDA, "tensor map A");
+  if (b_mn) {
+    if (!make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 128, n, n, 128, 64, true))
+      return fail(SKR_E_CUDA, "tensor map B");
+  } else {
+    if (!make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, 128, 128, n, 64, true))
+      return fail(SKR_E_CUDA, "tensor map B");
+  }
+  const int smem = 65536 + 64 + 1024;
+  cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  selftest_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(ta, tb, (const __nv_bfloat16*)A, C, variant, n);
+  return launch_status("selftest_kernel");
+}

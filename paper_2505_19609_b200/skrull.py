@@ -1,0 +1,301 @@
+"""Thin ctypes binding of libskrull.so (include/skrull.h): same names, marshalling only.
+
+Host planner calls take Python sequences / numpy arrays and return numpy arrays. Device calls
+take torch tensors (device memory) and use the current torch CUDA stream unless `stream` is
+given. Every non-OK status raises SkrullError with skr_last_error()'s message. There is no
+fallback: if the library is missing this module fails to import.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libskrull.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2505_19609_b200.build`")
+
+_lib = C.CDLL(LIB_PATH)
+
+SKR_OK, SKR_E_ARG, SKR_E_SCHEDULE, SKR_E_GDS, SKR_E_BUDGET, SKR_E_PROFILE = range(6)
+SKR_E_OVERFLOW, SKR_E_CAPACITY, SKR_E_CUDA, SKR_E_NCCL, SKR_E_UNSUPPORTED = range(6, 11)
+SKR_BF16, SKR_FP32 = 0, 1
+
+i32, i64, f64, f32 = C.c_int32, C.c_int64, C.c_double, C.c_float
+P = C.POINTER
+vp = C.c_void_p
+
+
+class SkrullError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+
+
+class skr_model(C.Structure):
+    _fields_ = [("hidden", i64), ("kv_hidden", i64), ("pack_batch", i64)]
+
+
+class skr_fit(C.Structure):
+    _fields_ = [("slope", f64), ("intercept", f64)]
+
+
+class skr_cost(C.Structure):
+    _fields_ = [("comp", skr_fit), ("comm", skr_fit), ("mem", skr_fit), ("bytes_per_elem", f64),
+                ("dist_penalty", f64)]
+
+
+class skr_cluster(C.Structure):
+    _fields_ = [("cp", i32), ("dp", i32), ("bucket_tokens", i64), ("rollback", i32)]
+
+
+class skr_attn_shape(C.Structure):
+    _fields_ = [("hq", i32), ("hkv", i32), ("d", i32), ("dtype", i32), ("scale", f32)]
+
+
+class skr_segs(C.Structure):
+    _fields_ = [("cu_seqlens_q", vp), ("q_pos", vp), ("k_start", vp), ("k_len", vp), ("tiles", vp),
+                ("n_seg", i32), ("n_tiles", i32), ("row_begin", i32), ("row_end", i32)]
+
+
+def _sig(name, res, *args):
+    fn = getattr(_lib, name)
+    fn.restype = res
+    fn.argtypes = list(args)
+    return fn
+
+
+_lib.skr_last_error.restype = C.c_char_p
+_lib.skr_status_string.restype = C.c_char_p
+_lib.skr_status_string.argtypes = [i32]
+
+
+def _check(st):
+    if st != SKR_OK:
+        msg = _lib.skr_last_error().decode() or _lib.skr_status_string(st).decode()
+        raise SkrullError(st, msg)
+
+
+def _ptr(a, ctype):
+    return a.ctypes.data_as(P(ctype))
+
+
+def _tptr(t):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+def skr_abi_version() -> int:
+    return _sig("skr_abi_version", i32)()
+
+
+# ---------------------------------------------------------------------------- diagnostics
+def skr_selftest_umma(variant: int, n: int, A, B, Cout, stream=None):
+    fn = _sig("skr_selftest_umma", i32, i32, i32, vp, vp, vp, vp)
+    _check(fn(variant, n, _tptr(A), _tptr(B), _tptr(Cout), _stream(stream)))
+
+
+def exported_symbols():
+    """Names the header declares that this library exports (used by the ABI test)."""
+    out = []
+    for name in _declared_names():
+        try:
+            getattr(_lib, name)
+            out.append(name)
+        except AttributeError:
+            pass
+    return out
+
+
+def _declared_names():
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "skrull.h")
+    with open(hdr) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(skr_[a-z0-9_]+)\s*\(", text)))
+
+
+# ---------------------------------------------------------------------------- a1 cost model
+def _model(hidden, kv_hidden, pack_batch=1):
+    return skr_model(int(hidden), int(kv_hidden), int(pack_batch))
+
+
+def skr_flops(S, hidden, kv_hidden, pack_batch=1) -> int:
+    out = i64()
+    _check(_sig("skr_flops", i32, i64, P(skr_model), P(i64))(int(S), C.byref(_model(hidden, kv_hidden, pack_batch)),
+                                                            C.byref(out)))
+    return out.value
+
+
+def skr_volume(S, hidden, kv_hidden, pack_batch=1) -> int:
+    out = i64()
+    _check(_sig("skr_volume", i32, i64, P(skr_model), P(i64))(int(S), C.byref(_model(hidden, kv_hidden, pack_batch)),
+                                                             C.byref(out)))
+    return out.value
+
+
+def skr_t_comp(flops, slope, intercept) -> float:
+    return _sig("skr_t_comp", f64, f64, P(skr_fit))(float(flops), C.byref(skr_fit(slope, intercept)))
+
+
+def skr_t_comm(volume, slope, intercept) -> float:
+    return _sig("skr_t_comm", f64, f64, P(skr_fit))(float(volume), C.byref(skr_fit(slope, intercept)))
+
+
+def skr_fit_linear(x, y, min_x=0.0):
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    out = skr_fit()
+    _check(_sig("skr_fit_linear", i32, P(f64), P(f64), i32, f64, P(skr_fit))(
+        _ptr(x, f64), _ptr(y, f64), len(x), float(min_x), C.byref(out)))
+    return out.slope, out.intercept
+
+
+def skr_bucket_size(budget, slope, intercept) -> int:
+    out = i64()
+    _check(_sig("skr_bucket_size", i32, f64, P(skr_fit), P(i64))(float(budget), C.byref(skr_fit(slope, intercept)),
+                                                                C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------------------- a2/a3 schedulers
+def _cluster(cp, dp, bucket, rollback=True):
+    return skr_cluster(int(cp), int(dp), int(bucket), 1 if rollback else 0)
+
+
+def skr_dacp(lens, bucket, cp, hidden, kv_hidden, pack_batch=1, rollback=True):
+    """-> (assign int32[K], n_rollbacks). Raises SkrullError(SKR_E_SCHEDULE) with .fail_idx."""
+    L = np.ascontiguousarray(lens, np.int64)
+    A = np.zeros(len(L), np.int32)
+    nrb, fidx = i32(), i32()
+    st = _sig("skr_dacp", i32, P(i64), i32, P(skr_cluster), P(skr_model), P(i32), P(i32), P(i32))(
+        _ptr(L, i64), len(L), C.byref(_cluster(cp, 1, bucket, rollback)),
+        C.byref(_model(hidden, kv_hidden, pack_batch)), _ptr(A, i32), C.byref(nrb), C.byref(fidx))
+    if st != SKR_OK:
+        e = SkrullError(st, _lib.skr_last_error().decode())
+        e.fail_idx = fidx.value
+        raise e
+    return A, nrb.value
+
+
+def skr_eval_tdacp(lens, assign, bucket, cp, hidden, kv_hidden, comp, comm, pack_batch=1, bytes_per_elem=1.0,
+                   dist_penalty=1.0, mem=(1.0, 0.0)):
+    L = np.ascontiguousarray(lens, np.int64)
+    A = np.ascontiguousarray(assign, np.int32)
+    per = np.zeros(cp, np.float64)
+    tc, td, t, feas = f64(), f64(), f64(), i32()
+    cost = skr_cost(skr_fit(*comp), skr_fit(*comm), skr_fit(*mem), float(bytes_per_elem), float(dist_penalty))
+    _check(_sig("skr_eval_tdacp", i32, P(i64), P(i32), i32, P(skr_cluster), P(skr_model), P(skr_cost), P(f64),
+                P(f64), P(f64), P(f64), P(i32))(
+        _ptr(L, i64), _ptr(A, i32), len(L), C.byref(_cluster(cp, 1, bucket)),
+        C.byref(_model(hidden, kv_hidden, pack_batch)), C.byref(cost), _ptr(per, f64), C.byref(tc), C.byref(td),
+        C.byref(t), C.byref(feas)))
+    return dict(per_rank_time=per, comm_time=tc.value, dist_time=td.value, tdacp=t.value, feasible=bool(feas.value))
+
+
+def skr_lpt(lens, bins, hidden, kv_hidden, pack_batch=1):
+    L = np.ascontiguousarray(lens, np.int64)
+    B = np.zeros(len(L), np.int32)
+    _check(_sig("skr_lpt", i32, P(i64), i32, i32, P(skr_model), P(i32))(
+        _ptr(L, i64), len(L), int(bins), C.byref(_model(hidden, kv_hidden, pack_batch)), _ptr(B, i32)))
+    return B
+
+
+def skr_gds(lens, bucket, cp, dp, dp_rank, hidden, kv_hidden, pack_batch=1, rollback=True):
+    L = np.ascontiguousarray(lens, np.int64)
+    M = np.zeros(len(L), np.int32)
+    n = i32()
+    _check(_sig("skr_gds", i32, P(i64), i32, P(skr_cluster), P(skr_model), i32, P(i32), P(i32))(
+        _ptr(L, i64), len(L), C.byref(_cluster(cp, dp, bucket, rollback)),
+        C.byref(_model(hidden, kv_hidden, pack_batch)), int(dp_rank), _ptr(M, i32), C.byref(n)))
+    return M, n.value
+
+
+def skr_plan(lens, bucket, cp, dp, hidden, kv_hidden, pack_batch=1, rollback=True):
+    """-> dict(dp_of_seq, mb_of_seq, assign, n_mb_per_dp, n_rollbacks)."""
+    L = np.ascontiguousarray(lens, np.int64)
+    K = len(L)
+    dpo, mbo, asg = (np.zeros(K, np.int32) for _ in range(3))
+    nmb = np.zeros(dp, np.int32)
+    nrb = i32()
+    _check(_sig("skr_plan", i32, P(i64), i32, P(skr_cluster), P(skr_model), P(i32), P(i32), P(i32), P(i32),
+                P(i32))(
+        _ptr(L, i64), K, C.byref(_cluster(cp, dp, bucket, rollback)), C.byref(_model(hidden, kv_hidden, pack_batch)),
+        _ptr(dpo, i32), _ptr(mbo, i32), _ptr(asg, i32), _ptr(nmb, i32), C.byref(nrb)))
+    return dict(dp_of_seq=dpo, mb_of_seq=mbo, assign=asg, n_mb_per_dp=nmb, n_rollbacks=nrb.value)
+
+
+# ---------------------------------------------------------------------------- a4 packer
+def skr_pack_bounds(mb_lens, assign, cp, rank):
+    L = np.ascontiguousarray(mb_lens, np.int64)
+    A = np.ascontiguousarray(assign, np.int32)
+    v = [i32() for _ in range(7)]
+    _check(_sig("skr_pack_bounds", i32, P(i64), P(i32), i32, i32, i32, *([P(i32)] * 7))(
+        _ptr(L, i64), _ptr(A, i32), len(L), int(cp), int(rank), *[C.byref(x) for x in v]))
+    keys = ("n_seg", "n_dist_seg", "n_rows", "dist_rows", "pad_rows_P", "natural_rows", "n_chunks")
+    return dict(zip(keys, (x.value for x in v)))
+
+
+def skr_pack_rank(mb_lens, assign, cp, rank):
+    b = skr_pack_bounds(mb_lens, assign, cp, rank)
+    L = np.ascontiguousarray(mb_lens, np.int64)
+    A = np.ascontiguousarray(assign, np.int32)
+    ns, nr = b["n_seg"], b["n_rows"]
+    cu = np.zeros(ns + 1, np.int32)
+    qp, ks, kl, ss, sc = (np.zeros(ns, np.int32) for _ in range(5))
+    src = np.zeros(nr, np.int32)
+    _check(_sig("skr_pack_rank", i32, P(i64), P(i32), i32, i32, i32, *([P(i32)] * 7))(
+        _ptr(L, i64), _ptr(A, i32), len(L), int(cp), int(rank), _ptr(cu, i32), _ptr(qp, i32), _ptr(ks, i32),
+        _ptr(kl, i32), _ptr(ss, i32), _ptr(sc, i32), _ptr(src, i32)))
+    b.update(cu_seqlens_q=cu, q_pos=qp, k_start=ks, k_len=kl, seg_seq=ss, seg_chunk=sc, src_row=src)
+    return b
+
+
+def skr_pack_chunks(mb_lens, assign, cp):
+    b = skr_pack_bounds(mb_lens, assign, cp, 0)
+    L = np.ascontiguousarray(mb_lens, np.int64)
+    A = np.ascontiguousarray(assign, np.int32)
+    t = np.zeros((b["n_chunks"], 6), np.int32)
+    _check(_sig("skr_pack_chunks", i32, P(i64), P(i32), i32, i32, P(i32))(
+        _ptr(L, i64), _ptr(A, i32), len(L), int(cp), _ptr(t, i32)))
+    return t
+
+
+def _tiles(fn_name, cu, q_pos, k_len, n_seg, block):
+    cu = np.ascontiguousarray(cu, np.int32)
+    qp = np.ascontiguousarray(q_pos, np.int32)
+    n = i32()
+    cap = 0
+    for _ in range(2):
+        out = np.zeros(2 * max(cap, 1), np.int32)
+        if fn_name == "skr_tiles_fwd":
+            st = _sig(fn_name, i32, P(i32), P(i32), i32, i32, P(i32), i32, P(i32))(
+                _ptr(cu, i32), _ptr(qp, i32), int(n_seg), int(block), _ptr(out, i32), cap, C.byref(n))
+        else:
+            kl = np.ascontiguousarray(k_len, np.int32)
+            st = _sig(fn_name, i32, P(i32), P(i32), P(i32), i32, i32, P(i32), i32, P(i32))(
+                _ptr(cu, i32), _ptr(qp, i32), _ptr(kl, i32), int(n_seg), int(block), _ptr(out, i32), cap,
+                C.byref(n))
+        if st == SKR_OK:
+            return out[:2 * n.value].reshape(-1, 2)
+        if st != SKR_E_CAPACITY:
+            _check(st)
+        cap = n.value
+    raise SkrullError(SKR_E_CAPACITY, "tiles")
+
+
+def skr_tiles_fwd(cu, q_pos, n_seg, block_m):
+    return _tiles("skr_tiles_fwd", cu, q_pos, None, n_seg, block_m)
+
+
+def skr_tiles_bwd(cu, q_pos, k_len, n_seg, block_n):
+    return _tiles("skr_tiles_bwd", cu, q_pos, k_len, n_seg, block_n)

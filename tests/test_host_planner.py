@@ -1,0 +1,184 @@
+"""C-ABI host planner (libskrull.so) vs the independent oracle: bit-exact plans and tables.
+
+No GPU needed: these call only host entry points of the library.
+"""
+import os
+import random
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle.cost_model import Fit, Model, flops, volume
+from oracle.pack import pack_microbatch
+from oracle.schedule import GDSError, ScheduleError, dacp, eval_tdacp, gds, lpt, plan
+
+skrull = pytest.importorskip("paper_2505_19609_b200.skrull")
+
+SHAPES = [(896, 128), (3584, 512), (4096, 1024), (64, 16), (1, 1)]
+
+
+def test_abi_exports_every_declared_symbol():
+    declared = skrull._declared_names()
+    assert len(declared) > 30
+    missing = [n for n in declared if n not in skrull.exported_symbols()]
+    assert not missing, missing
+    assert skrull.skr_abi_version() >= 1
+
+
+def test_cost_model_matches_oracle():
+    for h, hkv in SHAPES:
+        for S in (0, 1, 17, 4096, 131072, 1_643_000):
+            assert skrull.skr_flops(S, h, hkv) == flops(S, Model(h, hkv))
+            assert skrull.skr_volume(S, h, hkv) == volume(S, Model(h, hkv))
+    with pytest.raises(skrull.SkrullError) as e:
+        skrull.skr_flops(2 ** 40, 4096, 1024)
+    assert e.value.status == skrull.SKR_E_OVERFLOW
+    assert skrull.skr_t_comp(0, 3, 9) == 0 and skrull.skr_t_comp(1000, 0.5, 10) == 510
+    assert skrull.skr_t_comm(0, 3, 9) == 0 and skrull.skr_t_comm(4, 1, 0) == 4
+    s, i = skrull.skr_fit_linear([1, 2, 3, 4], [7, 9, 11, 13])
+    assert abs(s - 2) < 1e-12 and abs(i - 5) < 1e-12
+    with pytest.raises(skrull.SkrullError):
+        skrull.skr_fit_linear([2], [80.62])
+    assert skrull.skr_bucket_size(210, 2, 10) == 100
+    with pytest.raises(skrull.SkrullError):
+        skrull.skr_bucket_size(10, 2, 10)
+
+
+def _lens(rng, K, mu=5.0, sigma=1.3, hi=20000):
+    return [int(min(hi, max(1, round(rng.lognormvariate(mu, sigma))))) for _ in range(K)]
+
+
+def test_dacp_bit_exact_fuzz():
+    rng = random.Random(11)
+    n_err = 0
+    for it in range(1500):
+        N = rng.choice([1, 2, 3, 4, 8])
+        K = rng.randint(0, 60)
+        h, hkv = rng.choice(SHAPES)
+        L = _lens(rng, K)
+        tot = sum(L)
+        C = rng.randint(max(1, (max(L) if L else 1) // N // 2), max(2, tot // N + 500))
+        rb = rng.random() < 0.85
+        try:
+            ref = dacp(L, C, N, Model(h, hkv), rb)
+        except ScheduleError as e:
+            n_err += 1
+            with pytest.raises(skrull.SkrullError) as ce:
+                skrull.skr_dacp(L, C, N, h, hkv, rollback=rb)
+            assert ce.value.status == skrull.SKR_E_SCHEDULE
+            assert ce.value.fail_idx == e.pos
+            continue
+        A, nrb = skrull.skr_dacp(L, C, N, h, hkv, rollback=rb)
+        assert list(A) == ref.assign, (L, C, N)
+        assert nrb == ref.n_rollbacks
+    assert 50 < n_err < 1400
+
+
+def test_eval_tdacp_matches_oracle():
+    rng = random.Random(12)
+    for _ in range(300):
+        N = rng.choice([1, 2, 4])
+        K = rng.randint(1, 12)
+        L = _lens(rng, K, hi=5000)
+        A = [rng.randint(-1, N - 1) for _ in range(K)]
+        C = rng.randint(1, 6000)
+        comp, comm = (1e-9, 3.0), (2e-6, 100.0)
+        r = skrull.skr_eval_tdacp(L, A, C, N, 896, 128, comp, comm, bytes_per_elem=2, dist_penalty=1.2)
+        o = eval_tdacp(L, A, C, N, Model(896, 128), Fit(*comp), Fit(*comm), 2, Fraction(6, 5))
+        assert r["feasible"] == o.feasible
+        assert abs(r["tdacp"] - float(o.tdacp)) <= 1e-9 * max(1.0, float(o.tdacp))
+        assert abs(r["comm_time"] - float(o.comm_time)) <= 1e-9 * max(1.0, float(o.comm_time))
+        np.testing.assert_allclose(r["per_rank_time"], [float(x) for x in o.per_rank_time], rtol=1e-9)
+
+
+def test_worked_tdacp_examples():
+    # 144 / 160 / 84 under identity fits, h = h_kv = b = 1
+    assert skrull.skr_eval_tdacp([4, 2, 2], [-1, 0, 1], 100, 2, 1, 1, (1, 0), (1, 0))["tdacp"] == 144
+    assert skrull.skr_eval_tdacp([4], [0], 100, 2, 1, 1, (1, 0), (1, 0))["tdacp"] == 160
+    assert skrull.skr_eval_tdacp([4], [-1], 100, 2, 1, 1, (1, 0), (1, 0))["tdacp"] == 84
+
+
+def test_lpt_gds_plan_bit_exact_fuzz():
+    rng = random.Random(13)
+    for _ in range(300):
+        N = rng.choice([1, 2, 4, 8])
+        ws = rng.choice([1, 2, 4])
+        K = rng.randint(1, 80)
+        h, hkv = rng.choice(SHAPES[:3])
+        L = _lens(rng, K)
+        C = rng.randint(max(1, max(L) // (2 * N)), max(L) + 4000)
+        m = Model(h, hkv)
+        assert list(skrull.skr_lpt(L, ws, h, hkv)) == lpt(L, ws, m)
+        try:
+            ref = plan(L, C, N, ws, m)
+        except (GDSError, ScheduleError):
+            with pytest.raises(skrull.SkrullError):
+                skrull.skr_plan(L, C, N, ws, h, hkv)
+            continue
+        p = skrull.skr_plan(L, C, N, ws, h, hkv)
+        assert list(p["dp_of_seq"]) == ref.dp_of_seq
+        assert list(p["mb_of_seq"]) == ref.mb_of_seq
+        assert list(p["assign"]) == ref.assign
+        assert list(p["n_mb_per_dp"]) == ref.n_mb
+        assert p["n_rollbacks"] == ref.n_rollbacks
+        for i in range(ws):
+            mbo, n = skrull.skr_gds(L, C, N, ws, i, h, hkv)
+            assert n == ref.n_mb[i]
+
+
+def test_toy_plan_through_abi(golden):
+    g = golden("toy_c1_plan.json")
+    p = skrull.skr_plan(g["lengths"], g["C"], g["N"], 1, g["hidden"], g["kv_hidden"])
+    assert list(p["assign"]) == g["assign"] and p["n_rollbacks"] == g["n_rollbacks"]
+    assert list(p["n_mb_per_dp"]) == [g["gds_init"]]
+    for j, key in enumerate(("rank0", "rank1")):
+        r = skrull.skr_pack_rank(g["lengths"], g["assign"], g["N"], j)
+        assert list(r["cu_seqlens_q"]) == g[key]["cu_seqlens_q"]
+        assert list(r["q_pos"]) == g[key]["q_pos"]
+        assert list(r["k_len"]) == g[key]["k_len"]
+        assert r["pad_rows_P"] == g["pad_rows_P"] and r["natural_rows"] == g["natural_rows"]
+
+
+def test_pack_bit_exact_fuzz():
+    rng = random.Random(14)
+    for _ in range(300):
+        N = rng.choice([1, 2, 3, 4, 8])
+        K = rng.randint(0, 40)
+        L = [rng.randint(0, 3000) for _ in range(K)]
+        A = [rng.randint(-1, N - 1) for _ in range(K)]
+        ref = pack_microbatch(L, A, N)
+        t = skrull.skr_pack_chunks(L, A, N)
+        assert len(t) == len(ref.chunks)
+        for row, c in zip(t, ref.chunks):
+            assert list(row) == [c["seq"], c["c"], c["owner"], c["gathered_row"], c["natural_row"], c["len"]]
+        for j in range(N):
+            r = skrull.skr_pack_rank(L, A, N, j)
+            o = ref.ranks[j]
+            assert list(r["cu_seqlens_q"]) == o.cu_seqlens_q
+            assert list(r["q_pos"]) == o.q_pos
+            assert list(r["k_start"]) == o.k_start
+            assert list(r["k_len"]) == o.k_len
+            assert list(r["seg_seq"]) == o.seg_seq
+            assert list(r["seg_chunk"]) == o.seg_chunk
+            assert list(r["src_row"]) == o.src_row
+            assert r["dist_rows"] == o.dist_rows and r["pad_rows_P"] == ref.pad_rows
+            assert r["n_dist_seg"] == o.n_dist_seg
+
+
+def test_tiles_cover_work_once_and_are_lpt_ordered():
+    rng = random.Random(15)
+    for _ in range(50):
+        n = rng.randint(0, 20)
+        ql = [rng.randint(0, 700) for _ in range(n)]
+        qp = [rng.randint(0, 500) for _ in range(n)]
+        cu = np.concatenate([[0], np.cumsum(ql)]).astype(np.int32)
+        kl = [a + b for a, b in zip(qp, ql)]
+        tf = skrull.skr_tiles_fwd(cu, qp, n, 128)
+        assert sorted(map(tuple, tf)) == sorted((s, t) for s in range(n) for t in range(-(-ql[s] // 128)))
+        w = [qp[s] + min(ql[s], (t + 1) * 128) for s, t in tf]
+        assert w == sorted(w, reverse=True)
+        tb = skrull.skr_tiles_bwd(cu, qp, kl, n, 128)
+        assert sorted(map(tuple, tb)) == sorted((s, t) for s in range(n) if ql[s] > 0
+                                                for t in range(-(-kl[s] // 128)))
