@@ -1,0 +1,318 @@
+// Row a7: packed varlen causal attention forward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Work unit (CTA): one 128-row query tile of one segment x two q-heads of the same KV group
+// (GQA, R30), so each K/V tile is loaded once into shared memory and feeds both heads.
+// Warp roles (320 threads):
+//   warps 0-3  softmax warpgroup A (head ha), thread t owns query row t of the tile
+//   warps 4-7  softmax warpgroup B (head hb = ha + 1, if it exists in the group)
+//   warp 8     TMA producer: Q tiles once, then a ring of K/V tiles (SW128, 64-col boxes)
+//   warp 9     MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM
+// TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+d) O_B [384,384+d).
+// Softmax: S row read with tcgen05.ld (no shuffles: one thread = one row), exp2 with the scale
+// folded in, running max kept in log2 units and O rescaled in TMEM only when the max grows by
+// more than 8 (exact: the final normalisation uses the same reference max), P written as bf16 into
+// swizzled smem (K-major A operand of the PV MMA). Causal: only KV tiles up to the tile's last
+// query are visited (bottom-right aligned with q_pos, R23); the diagonal tiles are masked.
+#include "attn_common.cuh"
+#include "device.cuh"
+#include "sm100.cuh"
+#include "tma.h"
+
+namespace skr {
+namespace fwd {
+
+constexpr int BM = 128, BN = 128;
+constexpr int kThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct Cfg {
+  static constexpr int kChunks = D / 64;                 // 64-col SW128 boxes per row
+  static constexpr int kQBytes = BM * D * 2;             // one Q tile
+  static constexpr int kKVBytes = BN * D * 2;            // one K or V tile
+  static constexpr int kUnits = D == 128 ? 3 : 4;        // K/V ring depth (units of one tile)
+  static constexpr int kPBytes = BM * BN * 2;            // P tile (bf16)
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffKV = 2 * kQBytes;
+  static constexpr int kOffP = kOffKV + kUnits * kKVBytes;
+  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  static constexpr int kSmem = kOffBar + 256 + 1024;    // + barriers + alignment slack
+};
+
+struct Bars {
+  uint64_t q_full;
+  uint64_t kv_full[4], kv_empty[4];
+  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint32_t tmem_base;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
+                    float* __restrict__ lse, int pairs_per_group) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  // ---- work unit
+  const int pair = blockIdx.x;
+  const int grp = a.hq / a.hkv;
+  const int g = pair / pairs_per_group, p = pair % pairs_per_group;
+  const int ha = g * grp + 2 * p;
+  const int hb = (2 * p + 1 < grp) ? ha + 1 : -1;
+  const int seg = a.tiles[2 * blockIdx.y], tile = a.tiles[2 * blockIdx.y + 1];
+  const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
+  const int r0 = cu0 + tile * BM;                       // first packed query row of the tile
+  const int n_valid = min(BM, cu1 - r0);
+  const int qp0 = a.q_pos[seg] + tile * BM;             // position of the tile's first query
+  const int k_hi = qp0 + n_valid;                       // keys visible to the last valid query
+  const int n_kv = (k_hi + BN - 1) / BN;
+  const int kst = a.k_start[seg];
+  const int nq = hb >= 0 ? 2 : 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
+    for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars->s_full[s], 1);
+      mbar_init(&bars->p_full[s], 128);
+      mbar_init(&bars->pv_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 8) {
+    // ================= TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_expect_tx(&bars->q_full, nq * C::kQBytes);
+      for (int s = 0; s < nq; ++s) {
+        const int h = s == 0 ? ha : hb;
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_2d(smem + C::kOffQ + s * C::kQBytes + c * (BM * 128), &tm_q, &bars->q_full, h * D + c * 64, r0);
+      }
+      int it = 0;
+      for (int j = 0; j < n_kv; ++j) {
+        for (int kv = 0; kv < 2; ++kv, ++it) {
+          const int u = it % C::kUnits;
+          mbar_wait(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+          mbar_expect_tx(&bars->kv_full[u], C::kKVBytes);
+          uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_2d(dst + c * (BN * 128), kv == 0 ? &tm_k : &tm_v, &bars->kv_full[u], g * D + c * 64,
+                        kst + j * BN);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0);   // S = Q K^T   (both K-major)
+      const uint32_t id_o = idesc_bf16_f32(BM, D, 0, 1);    // O += P V    (V is MN-major)
+      const uint32_t sQ = smem_u32(smem + C::kOffQ), sKV = smem_u32(smem + C::kOffKV);
+      const uint32_t sP = smem_u32(smem + C::kOffP);
+      auto issue_s = [&](int s, uint32_t k_addr) {
+        const uint32_t q_addr = sQ + s * C::kQBytes;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * (BM * 128) + (k % 4) * 32;
+          const uint32_t koff = (k / 4) * (BN * 128) + (k % 4) * 32;
+          umma_f16(tmem + s * 128, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + koff, 16, 1024), id_s,
+                   k > 0);
+        }
+        umma_commit(&bars->s_full[s]);
+      };
+      auto issue_pv = [&](int s, uint32_t v_addr, bool acc) {
+        const uint32_t p_addr = sP + s * C::kPBytes;
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) {
+          const uint32_t poff = (k / 4) * (BM * 128) + (k % 4) * 32;
+          umma_f16(tmem + 256 + s * 128, sdesc_sw128(p_addr + poff, 16, 1024),
+                   sdesc_sw128(v_addr + k * 2048, BN * 128, 1024), id_o, acc || k > 0);
+        }
+        umma_commit(&bars->pv_done[s]);
+      };
+      mbar_wait(&bars->q_full, 0);
+      tc_fence_after();
+      // tile 0: S for both heads
+      int it = 0;
+      {
+        const int u = it % C::kUnits;
+        mbar_wait(&bars->kv_full[u], (it / C::kUnits) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = sKV + u * C::kKVBytes;
+        for (int s = 0; s < nq; ++s) issue_s(s, k_addr);
+        umma_commit(&bars->kv_empty[u]);
+        ++it;
+      }
+      for (int j = 1; j <= n_kv; ++j) {
+        // V of tile j-1
+        const int uv = it % C::kUnits;
+        mbar_wait(&bars->kv_full[uv], (it / C::kUnits) & 1);
+        ++it;
+        const uint32_t v_addr = sKV + uv * C::kKVBytes;
+        int uk = -1;
+        uint32_t k_addr = 0;
+        if (j < n_kv) {
+          uk = it % C::kUnits;
+          mbar_wait(&bars->kv_full[uk], (it / C::kUnits) & 1);
+          ++it;
+          k_addr = sKV + uk * C::kKVBytes;
+        }
+        tc_fence_after();
+        for (int s = 0; s < nq; ++s) {
+          mbar_wait(&bars->p_full[s], (j - 1) & 1);     // P_s(j-1) in smem, S_s(j-1) consumed, O_s corrected
+          tc_fence_after();
+          issue_pv(s, v_addr, j > 1);
+          if (j < n_kv) issue_s(s, k_addr);
+        }
+        umma_commit(&bars->kv_empty[uv]);
+        if (uk >= 0) umma_commit(&bars->kv_empty[uk]);
+      }
+    }
+  } else {
+    // ================= softmax warpgroups
+    const int s = warp / 4;                 // 0 -> head A, 1 -> head B
+    const int h = s == 0 ? ha : hb;
+    if (h >= 0) {
+      const int row = (warp % 4) * 32 + lane;  // TMEM lane == query row of the tile
+      const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
+      const uint32_t tS = tmem + lane_base + s * 128;
+      const uint32_t tO = tmem + lane_base + 256 + s * 128;
+      const int qp = qp0 + row;                // this row's query position
+      const float sl2 = a.scale * 1.4426950408889634f;
+      float m_ref = -INFINITY, l = 0.f;
+      uint8_t* sP = smem + C::kOffP + s * C::kPBytes;
+      const uint32_t sP_u32 = smem_u32(sP);
+      for (int j = 0; j < n_kv; ++j) {
+        mbar_wait(&bars->s_full[s], j & 1);
+        tc_fence_after();
+        float x[BN];
+#pragma unroll
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tS + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[c + i] = __uint_as_float(r[i]);
+        }
+        const int kv0 = j * BN;
+        if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
+#pragma unroll
+          for (int i = 0; i < BN; ++i)
+            if (kv0 + i > qp) x[i] = -INFINITY;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < BN; ++i) mx = fmaxf(mx, x[i]);
+        const float m_new = fmaxf(m_ref, mx * sl2);
+        // P_s(j-1) consumed and O_s(j-1) accumulated before P / O are touched again
+        if (j > 0) {
+          mbar_wait(&bars->pv_done[s], (j - 1) & 1);
+          tc_fence_after();
+        }
+        if (m_new > m_ref + kRescaleThreshold || j == 0) {
+          const float alpha = j == 0 ? 0.f : ex2(m_ref - m_new);
+          if (j > 0) {
+#pragma unroll
+            for (int c = 0; c < D; c += 16) {
+              uint32_t r[16];
+              tmem_ld16(tO + c, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              tmem_st16(tO + c, r);
+            }
+            tmem_wait_st();
+          }
+          l *= alpha;
+          m_ref = m_new;
+        }
+        // P = exp2(S * scale * log2e - m_ref), row sum, bf16 into swizzled smem (K-major A operand)
+        const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) {
+          float pv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            pv[i] = ex2(fmaf(x[c + i], sl2, neg_m));
+            l += pv[i];
+          }
+          const uint32_t addr = sP_u32 + (c / 64) * (BM * 128) + sw128_off(row, c % 64);
+          st_shared_v4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
+                       pack_bf16(pv[6], pv[7]));
+        }
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full[s]);
+      }
+      // ---- epilogue: O / l -> bf16, LSE
+      mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+      const bool store = row < n_valid;
+      __nv_bfloat16* orow = out + ((size_t)(r0 + row) * a.hq + h) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tO + c, r);
+        tmem_wait_ld();
+        if (store) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c + i) = v;
+          }
+        }
+      }
+      if (store) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace fwd
+
+skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k, const void* v, void* o, float* lse,
+                          int n_q_rows, int n_kv_rows, cudaStream_t st) {
+  if (a.n_tiles == 0) return SKR_OK;
+  CUtensorMap tq, tk, tv;
+  const uint64_t qcols = (uint64_t)a.hq * d, kcols = (uint64_t)a.hkv * d;
+  if (!make_tmap_2d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, fwd::BM, 64, true) ||
+      !make_tmap_2d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, fwd::BN, 64, true) ||
+      !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, fwd::BN, 64, true))
+    return fail(SKR_E_CUDA, "attn fwd: tensor map encode failed");
+  const int grp = a.hq / a.hkv;
+  const int ppg = (grp + 1) / 2;
+  dim3 grid(a.hkv * ppg, a.n_tiles);
+  if (d == 128) {
+    constexpr int smem = fwd::Cfg<128>::kSmem;
+    cudaFuncSetAttribute(fwd::attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    fwd::attn_fwd_kernel<128><<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
+  } else if (d == 64) {
+    constexpr int smem = fwd::Cfg<64>::kSmem;
+    cudaFuncSetAttribute(fwd::attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    fwd::attn_fwd_kernel<64><<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
+  } else {
+    return fail(SKR_E_UNSUPPORTED, "bf16 attention supports d in {64, 128}");
+  }
+  return launch_status("attn_fwd_kernel");
+}
+
+}  // namespace skr

@@ -299,3 +299,138 @@ def skr_tiles_fwd(cu, q_pos, n_seg, block_m):
 
 def skr_tiles_bwd(cu, q_pos, k_len, n_seg, block_n):
     return _tiles("skr_tiles_bwd", cu, q_pos, k_len, n_seg, block_n)
+
+
+# ---------------------------------------------------------------------------- a5-a9 device
+def attn_shape(hq, hkv, d, dtype=SKR_BF16, scale=None):
+    return skr_attn_shape(int(hq), int(hkv), int(d), int(dtype), float(scale if scale is not None else d ** -0.5))
+
+
+def skr_attn_block_m(shape) -> int:
+    return _sig("skr_attn_block_m", i32, P(skr_attn_shape))(C.byref(shape))
+
+
+def skr_attn_block_n(shape) -> int:
+    return _sig("skr_attn_block_n", i32, P(skr_attn_shape))(C.byref(shape))
+
+
+def skr_attn_bwd_ws_bytes(shape, n_q_rows) -> int:
+    return _sig("skr_attn_bwd_ws_bytes", C.c_size_t, P(skr_attn_shape), i32)(C.byref(shape), int(n_q_rows))
+
+
+class DeviceSegs:
+    """Device copy of one segment class's tables (+ work list); keeps the tensors alive."""
+
+    def __init__(self, cu, q_pos, k_start, k_len, tiles, row_begin=None, row_end=None, device="cuda"):
+        import torch
+        cu = np.ascontiguousarray(cu, np.int32)
+        self.n_seg = len(cu) - 1
+        t = lambda x: torch.as_tensor(np.ascontiguousarray(x, np.int32)).to(device)  # noqa: E731
+        self.cu, self.q_pos, self.k_start, self.k_len = t(cu), t(q_pos), t(k_start), t(k_len)
+        self.tiles = t(np.asarray(tiles, np.int32).reshape(-1))
+        self.n_tiles = len(self.tiles) // 2
+        self.row_begin = int(cu[0]) if row_begin is None else int(row_begin)
+        self.row_end = int(cu[-1]) if row_end is None else int(row_end)
+
+    def struct(self):
+        return skr_segs(self.cu.data_ptr(), self.q_pos.data_ptr(), self.k_start.data_ptr(), self.k_len.data_ptr(),
+                        self.tiles.data_ptr() if self.n_tiles else 0, self.n_seg, self.n_tiles, self.row_begin,
+                        self.row_end)
+
+
+def make_segs(shape, cu, q_pos, k_start, k_len, kind="fwd", device="cuda"):
+    """Host work list (skr_tiles_fwd / skr_tiles_bwd) + device tables for one segment class."""
+    n = len(cu) - 1
+    if kind == "fwd":
+        tiles = skr_tiles_fwd(cu, q_pos, n, skr_attn_block_m(shape))
+    else:
+        tiles = skr_tiles_bwd(cu, q_pos, k_len, n, skr_attn_block_n(shape))
+    return DeviceSegs(cu, q_pos, k_start, k_len, tiles, device=device)
+
+
+def skr_attn_fwd(shape, segs: DeviceSegs, q, k, v, o, lse, stream=None):
+    fn = _sig("skr_attn_fwd", i32, P(skr_attn_shape), P(skr_segs), vp, vp, vp, vp, vp, i32, i32, vp)
+    g = segs.struct()
+    _check(fn(C.byref(shape), C.byref(g), _tptr(q), _tptr(k), _tptr(v), _tptr(o), _tptr(lse), q.shape[0], k.shape[0],
+              _stream(stream)))
+
+
+def skr_attn_bwd(shape, segs: DeviceSegs, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate, ws, stream=None):
+    fn = _sig("skr_attn_bwd", i32, P(skr_attn_shape), P(skr_segs), vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32,
+              vp, C.c_size_t, vp)
+    g = segs.struct()
+    _check(fn(C.byref(shape), C.byref(g), _tptr(q), _tptr(k), _tptr(v), _tptr(o), _tptr(dout), _tptr(lse), _tptr(dq),
+              _tptr(dk), _tptr(dv), int(kv_accumulate), q.shape[0], k.shape[0], _tptr(ws),
+              ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def _rowbytes(t):
+    return t[0].numel() * t.element_size() if t.shape[0] else 0
+
+
+def skr_pack_rows(src, src_row, dst, stream=None):
+    fn = _sig("skr_pack_rows", i32, vp, vp, i32, i32, vp, vp)
+    _check(fn(_tptr(src), _tptr(src_row), dst.shape[0], dst[0].numel() * dst.element_size() if dst.shape[0] else 16,
+              _tptr(dst), _stream(stream)))
+
+
+def skr_unpack_rows(src, src_row, dst, stream=None):
+    fn = _sig("skr_unpack_rows", i32, vp, vp, i32, i32, vp, vp)
+    _check(fn(_tptr(src), _tptr(src_row), src.shape[0], src[0].numel() * src.element_size() if src.shape[0] else 16,
+              _tptr(dst), _stream(stream)))
+
+
+def skr_gather_chunks(gathered, chunk_table, n_chunks, natural, stream=None):
+    fn = _sig("skr_gather_chunks", i32, vp, vp, i32, i32, vp, vp)
+    rb = natural[0].numel() * natural.element_size()
+    _check(fn(_tptr(gathered), _tptr(chunk_table), int(n_chunks), rb, _tptr(natural), _stream(stream)))
+
+
+def skr_scatter_chunks(natural, chunk_table, n_chunks, pad_rows_P, cp, rankmajor, stream=None):
+    fn = _sig("skr_scatter_chunks", i32, vp, vp, i32, i32, i32, i32, vp, vp)
+    rb = rankmajor[0].numel() * rankmajor.element_size()
+    _check(fn(_tptr(natural), _tptr(chunk_table), int(n_chunks), rb, int(pad_rows_P), int(cp), _tptr(rankmajor),
+              _stream(stream)))
+
+
+def skr_cast_f32_bf16(src, dst, stream=None):
+    fn = _sig("skr_cast_f32_bf16", i32, vp, vp, i64, vp)
+    _check(fn(_tptr(src), _tptr(dst), src.numel(), _stream(stream)))
+
+
+# ---------------------------------------------------------------------------- CP communicator
+class Comm:
+    """skr_comm wrapper; the NCCL unique id is broadcast over an existing torch process group."""
+
+    def __init__(self, nranks, rank, group=None):
+        import torch
+        import torch.distributed as dist
+        n = _sig("skr_nccl_id_bytes", i32)()
+        buf = (C.c_uint8 * n)()
+        if rank == 0:
+            _check(_sig("skr_nccl_get_id", i32, vp)(C.cast(buf, vp)))
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if nranks > 1:
+            dist.broadcast(t, src=0, group=group)
+        buf = (C.c_uint8 * n)(*t.tolist())
+        self.h = vp()
+        _check(_sig("skr_comm_create", i32, vp, i32, i32, P(vp))(C.cast(buf, vp), int(nranks), int(rank),
+                                                                  C.byref(self.h)))
+        self.nranks, self.rank = nranks, rank
+
+    def all_gather(self, send, recv, stream=None):
+        _check(_sig("skr_comm_all_gather", i32, vp, vp, vp, C.c_size_t, vp)(
+            self.h, _tptr(send), _tptr(recv), send.numel() * send.element_size(), _stream(stream)))
+
+    def reduce_scatter_f32(self, send, recv, stream=None):
+        _check(_sig("skr_comm_reduce_scatter_f32", i32, vp, vp, vp, C.c_size_t, vp)(
+            self.h, _tptr(send), _tptr(recv), recv.numel(), _stream(stream)))
+
+    def all_reduce_f32(self, buf, stream=None):
+        _check(_sig("skr_comm_all_reduce_f32", i32, vp, vp, C.c_size_t, vp)(
+            self.h, _tptr(buf), buf.numel(), _stream(stream)))
+
+    def close(self):
+        if self.h:
+            _sig("skr_comm_destroy", None, vp)(self.h)
+            self.h = vp()

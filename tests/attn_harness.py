@@ -1,0 +1,85 @@
+"""Test harness: build packed varlen inputs from per-sequence synthetic tensors, run the CUDA path
+through the C-ABI binding, and compare with the fp64 oracle sequence by sequence.
+
+Tolerances (BASELINE.json north_star; reading R34):
+  bf16: max |gpu - oracle| <= 2e-2 per tensor (O, dQ, dK, dV)
+  fp32: max |gpu - oracle| <= 1e-5 * max(1, max |oracle|)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle.attention import attn_bwd, attn_fwd
+from synth import seq_tensors
+
+BF16_TOL = 2e-2
+FP32_TOL = 1e-5
+
+
+def tol_ok(got, ref, fp32: bool):
+    err = float(np.max(np.abs(got - ref))) if ref.size else 0.0
+    bound = FP32_TOL * max(1.0, float(np.max(np.abs(ref))) if ref.size else 1.0) if fp32 else BF16_TOL
+    return err <= bound, err, bound
+
+
+def make_inputs(lens, hq, hkv, d, seed=0, bf16=True, sigma_qk=1.0):
+    return [seq_tensors(seed, i, int(S), hq, hkv, d, bf16=bf16, sigma_qk=sigma_qk) for i, S in enumerate(lens)]
+
+
+def oracle_seq(x, scale=None, bwd=True):
+    O, L = attn_fwd(x["q"], x["k"], x["v"], scale)
+    if not bwd:
+        return O, L, None, None, None
+    dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"], scale)
+    return O, L, dQ, dK, dV
+
+
+class Packed:
+    """One rank's packed layout: rows of local sequences and/or distributed chunks.
+
+    segs: list of (seq, q_lo, q_hi) query ranges; `kv` maps seq -> base row in the K/V buffer
+    the segment attends into (packed rows for locals, natural buffer rows for chunks).
+    """
+
+    def __init__(self, inputs, segs, kv_rows_of, kv_seqs, torch_dtype, device="cuda"):
+        import torch
+        self.inputs = inputs
+        self.segs = segs
+        hq, d = inputs[0]["q"].shape[1], inputs[0]["q"].shape[2]
+        hkv = inputs[0]["k"].shape[1]
+        rows = sum(hi - lo for _, lo, hi in segs)
+        q = np.zeros((rows, hq, d), np.float32)
+        do = np.zeros_like(q)
+        cu = [0]
+        q_pos, k_start, k_len = [], [], []
+        for s, lo, hi in segs:
+            r = cu[-1]
+            q[r:r + hi - lo] = inputs[s]["q"][lo:hi]
+            do[r:r + hi - lo] = inputs[s]["do"][lo:hi]
+            cu.append(r + hi - lo)
+            q_pos.append(lo)
+            k_start.append(kv_rows_of[s])
+            k_len.append(hi)
+        n_kv = sum(len(inputs[s]["k"]) for s in kv_seqs) if kv_seqs else 0
+        k = np.zeros((max(n_kv, 1), hkv, d), np.float32)
+        v = np.zeros_like(k)
+        for s in kv_seqs:
+            b = kv_rows_of[s]
+            k[b:b + len(inputs[s]["k"])] = inputs[s]["k"]
+            v[b:b + len(inputs[s]["v"])] = inputs[s]["v"]
+        self.cu, self.q_pos, self.k_start, self.k_len = cu, q_pos, k_start, k_len
+        t = lambda a: torch.from_numpy(a).to(device=device, dtype=torch_dtype).contiguous()  # noqa: E731
+        self.q, self.k, self.v, self.do = t(q), t(k), t(v), t(do)
+        self.rows = rows
+        self.n_kv = k.shape[0]
+
+
+def local_pack(inputs, torch_dtype):
+    """All sequences local on one rank: packed rows = concatenation, K/V = the same rows."""
+    segs, base, r = [], {}, 0
+    for s, x in enumerate(inputs):
+        S = len(x["q"])
+        segs.append((s, 0, S))
+        base[s] = r
+        r += S
+    return Packed(inputs, segs, base, list(range(len(inputs))), torch_dtype)
