@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Bench: DACP/GDS-scheduled packed varlen causal attention fwd+bwd on B200 (the Skrull hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+
+One step = one pass of the whole hot path over one global batch: for
+every GDS micro-batch of this rank, pack Q/K/V (a5), K/V all-gather + reorder for distributed
+sequences (a6, N>1), attention forward local-then-distributed (a7), pack dO, attention backward
+distributed-then-local (a8), dK/dV reduce-scatter + cast (a9, N>1). The host plan (a1-a4, the
+paper's "near-zero overhead" DataLoader step) is computed once per global batch before the
+timed region and reported as `plan_us`.
+
+Metric (BASELINE.json): useful causal attention TFLOP/s fwd+bwd = sum_seq 14*d*Hq*S(S+1)/2 (R32)
+divided by the step time (max over ranks), whole-job aggregate. Inputs (Q, K, V, dO of the batch
+plus activations) exceed the 126 MB L2, so no explicit flush is done between steps.
+
+Rank 0 prints ONE JSON line. Under torchrun (N>1) every rank is one CP rank of a single CP group
+(DP = 1) and the workload is weak-scaled: N x the N=1 batch, C per rank fixed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS  # noqa: E402
+from synth.configs import Shape  # noqa: E402
+
+METRIC = "useful causal attn TFLOP/s fwd+bwd"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, help="workload (default: C2, weak-scaled by N)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workload
+def workload(args, world):
+    """Global batch lengths, shape, CP degree and BucketSize for this run."""
+    name = args.config or "C2"
+    cfg = CONFIGS[name]
+    if name == "C2":
+        # weak scaling of configs[1]: N x (63 long-tail + one 32K) sequences, one CP group of N.
+        # For N >= 2 the BucketSize is set below the longest sequence (R33) so DACP shards it.
+        lens = np.concatenate([cfg.lengths(args.seed + r) for r in range(world)])
+        bucket = cfg.bucket if world == 1 else 24576
+    else:
+        lens = cfg.lengths(args.seed)
+        bucket = cfg.bucket
+        if cfg.cp != world:
+            raise SystemExit(f"config {name} is for CP={cfg.cp}, launched with {world} ranks")
+    return name, cfg, np.asarray(lens, np.int64), cfg.shape, world, bucket
+
+
+def useful_flops(lens, shape: Shape, part="fwdbwd"):
+    pairs = sum(int(S) * (int(S) + 1) // 2 for S in lens)
+    per = {"fwd": 4, "bwd": 10, "fwdbwd": 14}[part]
+    return per * shape.d * shape.hq * pairs
+
+
+def rank_pairs(mb_lens, assign, cp, rank):
+    tot = 0
+    for S, a in zip(mb_lens, assign):
+        S = int(S)
+        if a == rank:
+            tot += S * (S + 1) // 2
+        elif a == -1:
+            for c in (rank, 2 * cp - 1 - rank):
+                lo, hi = c * S // (2 * cp), (c + 1) * S // (2 * cp)
+                tot += hi * (hi + 1) // 2 - lo * (lo + 1) // 2
+    return tot
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+def cpu_oracle_sample(lens, shape: Shape, seconds: float, seed: int = 0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: sequences taken
+    shortest-first until `seconds` of CPU work. Returns (TFLOP/s, n_seqs, tokens, wall_s)."""
+    from oracle.attention import attn_bwd, attn_fwd
+    from synth import seq_tensors
+    order = np.argsort(lens, kind="stable")
+    done_flops, n, toks, t_used = 0, 0, 0, 0.0
+    for k in order:
+        S = int(lens[k])
+        x = seq_tensors(seed, int(k), S, shape.hq, shape.hkv, shape.d)
+        t0 = time.perf_counter()
+        attn_fwd(x["q"], x["k"], x["v"])
+        attn_bwd(x["q"], x["k"], x["v"], x["do"])
+        t_used += time.perf_counter() - t0
+        done_flops += useful_flops([S], shape)
+        n += 1
+        toks += S
+        if t_used >= seconds:
+            break
+    return done_flops / t_used / 1e12, n, toks, t_used
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return 0
+    name, cfg, lens, shape, cp, bucket = workload(args, world)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    times, flops_done = [], 0
+    sample = None
+    for i in range(args.warmup + args.steps):
+        v, n, toks, t = cpu_oracle_sample(lens, shape, per_step, args.seed)
+        if i >= args.warmup:
+            times.append(t)
+            flops_done = v * t * 1e12
+            sample = f"{n} shortest sequences of the batch ({toks} tokens), fp64 naive attention fwd+bwd"
+    t = float(np.mean(times))
+    value = flops_done / t / 1e12
+    cores = len(os.sched_getaffinity(0))
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": name, "shape": f"Hq={shape.hq} Hkv={shape.hkv} d={shape.d}", "cp": cp,
+                      "bucket": bucket, "global_batch": int(len(lens))},
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_19609_b200 import skrull as sk
+    from paper_2505_19609_b200.runtime import RankStep
+
+    name, cfg, lens, shp, cp, bucket = workload(args, world)
+    shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
+    h, hkv = shp.hidden, shp.kv_hidden
+
+    # ---- a1-a4: host plan (every rank computes the identical plan)
+    t0 = time.perf_counter()
+    plan = sk.skr_plan(lens, bucket, cp, 1, h, hkv)
+    plan_us = (time.perf_counter() - t0) * 1e6
+    n_mb = int(plan["n_mb_per_dp"][0])
+    mbs = []
+    for j in range(n_mb):
+        idx = np.nonzero(plan["mb_of_seq"] == j)[0]
+        mbs.append((lens[idx], plan["assign"][idx]))
+
+    comm = sk.Comm(world, rank) if world > 1 else None
+    side = torch.cuda.Stream(priority=-1)
+    steps = []
+    g = torch.Generator(device="cuda")
+    for j, (ml, ma) in enumerate(mbs):
+        rs = RankStep(shape, ml, ma, cp, rank)
+        g.manual_seed(args.seed * 1_000_003 + rank * 1009 + j)
+        R = max(rs.rows, 1)
+        src = {k: torch.randn(R, hh, shp.d, device="cuda", generator=g).to(torch.bfloat16)
+               for k, hh in (("q", shp.hq), ("k", shp.hkv), ("v", shp.hkv), ("do", shp.hq))}
+        steps.append((rs, src))
+
+    fwd_ev, bwd_ev = [], []
+
+    def one_step(record=False):
+        for rs, src in steps:
+            if record:
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record()
+            rs.forward(src["q"], src["k"], src["v"], comm, side)
+            if record:
+                e1.record()
+            rs.backward(src["do"], comm, side)
+            if record:
+                e2.record()
+                fwd_ev.append((e0, e1))
+                bwd_ev.append((e1, e2))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        one_step()
+    torch.cuda.synchronize()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    start.record()
+    for _ in range(args.steps):
+        one_step()
+    end.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    my_ms = start.elapsed_time(end) / args.steps
+
+    # per-phase timing pass (separate from the headline timing; events around fwd / bwd)
+    fwd_ev.clear(), bwd_ev.clear()
+    for _ in range(max(2, min(args.steps, 5))):
+        one_step(record=True)
+    torch.cuda.synchronize()
+    nrep = max(2, min(args.steps, 5))
+    fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / nrep
+    bwd_ms = sum(a.elapsed_time(b) for a, b in bwd_ev) / nrep
+
+    # ---- e2e: host pinned inputs -> device, step, gradients back to host
+    e2e = None
+    if not args.no_e2e:
+        host = [{k: v.cpu().pin_memory() for k, v in src.items()} for _, src in steps]
+        outs = [{k: torch.empty(getattr(rs, k)[:rs.rows].shape, dtype=torch.bfloat16).pin_memory()
+                 for k in ("dq", "dk", "dv")} for rs, _ in steps]
+        h2d = sum(t.numel() * t.element_size() for hs in host for t in hs.values())
+        d2h = sum(t.numel() * t.element_size() for o in outs for t in o.values())
+
+        def e2e_step():
+            for (rs, src), hs, o in zip(steps, host, outs):
+                for k in src:
+                    src[k].copy_(hs[k], non_blocking=True)
+                rs.forward(src["q"], src["k"], src["v"], comm, side)
+                rs.backward(src["do"], comm, side)
+                for k in o:
+                    o[k].copy_(getattr(rs, k)[:rs.rows], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        s2, e2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e2_.record()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = s2.elapsed_time(e2_) / args.steps
+        e2e = (e2e_ms, h2d, d2h)
+
+    # ---- reduce over ranks: max (headline), per-rank list (imbalance)
+    vals = torch.tensor([my_ms, fwd_ms, bwd_ms, e2e[0] if e2e else 0.0], device="cuda", dtype=torch.float64)
+    if world > 1:
+        allv = [torch.zeros_like(vals) for _ in range(world)]
+        dist.all_gather(allv, vals)
+        allv = torch.stack(allv).cpu().numpy()
+    else:
+        allv = vals.cpu().numpy()[None]
+    step_ms = float(allv[:, 0].max())
+    total_flops = useful_flops(lens, shp)
+    value = total_flops / (step_ms * 1e-3) / 1e12
+
+    if rank == 0:
+        peaks, which = measured_peaks()
+        # dominant kernel: forward or backward attention call of the local class at N=1
+        # (algorithmic flops of this rank: 4 / 10 * d * Hq per causal pair it computes)
+        my_pairs = sum(rank_pairs(ml, ma, cp, rank) for ml, ma in mbs)
+        fwd_fl, bwd_fl = 4 * shp.d * shp.hq * my_pairs, 10 * shp.d * shp.hq * my_pairs
+        dom = ("bwd", bwd_fl, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", fwd_fl, fwd_ms)
+        achieved = dom[1] / (dom[2] * 1e-3) / 1e12
+        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+        gpu_launches = args.steps * sum(rs.launches_per_step() for rs, _ in steps)
+        cpu = None
+        if not args.no_cpu_baseline:
+            v, n, toks, t = cpu_oracle_sample(lens, shp, args.cpu_seconds, args.seed)
+            cpu = {"value": v, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                   "sample": f"{n} shortest sequences ({toks} tokens) of the batch, fp64 numpy fwd+bwd, {t:.1f} s"}
+        mean_rank = float(allv[:, 0].mean())
+        plan_pairs = [[rank_pairs(ml, ma, cp, r) for r in range(cp)] for ml, ma in mbs]
+        floor = sum(max(p) for p in plan_pairs) / max(1e-9, sum(sum(p) / cp for p in plan_pairs))
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": name, "desc": cfg.note,
+                       "shape": f"Hq={shp.hq} Hkv={shp.hkv} d={shp.d}", "global_batch": int(len(lens)),
+                       "tokens": int(lens.sum()), "max_seq_len": int(lens.max()), "cp": cp, "dp": 1,
+                       "bucket_tokens": int(bucket), "micro_batches": n_mb,
+                       "distributed_seqs": int((plan["assign"] == -1).sum()),
+                       "rollbacks": int(plan["n_rollbacks"]),
+                       "l2": "inputs larger than L2 (no flush)", "parallelism": f"cp{cp}"},
+            "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]}", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{which} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
+            "cpu_baseline": cpu,
+            "e2e": None if e2e is None else {"value": total_flops / (float(allv[:, 3].max()) * 1e-3) / 1e12,
+                                             "unit": "TFLOP/s", "h2d_bytes_per_step": e2e[1],
+                                             "d2h_bytes_per_step": e2e[2]},
+            "gpu_launches": gpu_launches,
+            "clocks": clocks,
+            "max_mean_rank_time": step_ms / mean_rank,
+            "plan_floor": floor,
+            "plan_us": plan_us,
+            "fwd_ms": float(allv[:, 1].max()), "bwd_ms": float(allv[:, 2].max()),
+        }
+        print(json.dumps(out), flush=True)
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,14 +1,471 @@
-// Row a8: packed varlen causal attention backward on sm_100a (tcgen05). [in progress]
+// Row a8: packed varlen causal attention backward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Plain definition (oracle/attention.py): P = exp(scale QK^T - LSE), dV = P^T dO,
+// dP = dO V^T, D = rowsum(dO o O), dS = P o (dP - D), dQ = scale dS K, dK = scale dS^T Q;
+// GQA sums dK/dV over the group's q-heads (R30).
+//
+// Work unit (CTA): one 128-key tile of one segment x one KV head g. It loops over the group's
+// q-heads and the query tiles that can see the key tile (causal: query position >= key position),
+// accumulating dK and dV in TMEM, so no cross-CTA reduction is needed for them.
+//   d = 128: query step BQ = 64.  TMEM: S^T[0,64) dP^T[64,128) dQ^T[128,192) dV[256,384) dK[384,512)
+//            dQ^T = K^T dS^T (M = d): thread = feature, reductions coalesced along d.
+//   d =  64: query step BQ = 128. TMEM: S^T[0,128) dP^T[128,256) dQ[256,320) dV[320,384) dK[384,448)
+//            dQ = dS K (M = query rows).
+// Warp roles (320 threads): warps 0-3 compute (thread = key row: P^T, dS^T from TMEM -> bf16
+// swizzled smem), warps 4-7 dQ reduction (TMEM -> fp32 red.global into the dQ accumulator),
+// warp 8 TMA producer (K, V once; Q/dO ring of 2 + LSE/D rows), warp 9 MMA issuer.
+// MMA order per step n:  S(n) dP(n) | P(n) -> dV(n) S(n+1) | dS(n) -> dK(n) dQ(n) dP(n+1)
+// so the tensor core works on one half of the step while the compute warpgroup does the other.
 #include "attn_common.cuh"
 #include "device.cuh"
+#include "sm100.cuh"
+#include "tma.h"
 
 namespace skr {
+namespace bwd {
+
+constexpr int BN = 128;  // key tile
+constexpr int kThreads = 320;
+
+template <int D>
+struct Cfg {
+  static constexpr int BQ = D == 128 ? 64 : 128;
+  static constexpr int kChunks = D / 64;
+  static constexpr int kKVBytes = BN * D * 2;
+  static constexpr int kQBytes = BQ * D * 2;
+  static constexpr int kPBytes = BN * BQ * 2;
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kKVBytes;
+  static constexpr int kOffQ = kOffV + kKVBytes;          // [2] stages
+  static constexpr int kOffDO = kOffQ + 2 * kQBytes;      // [2] stages
+  static constexpr int kOffP = kOffDO + 2 * kQBytes;
+  static constexpr int kOffDS = kOffP + kPBytes;
+  static constexpr int kOffAux = kOffDS + kPBytes;        // lse2[2][BQ], dd[2][BQ] fp32
+  static constexpr int kOffBar = kOffAux + 4 * BQ * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  // TMEM columns
+  static constexpr int tS = 0;
+  static constexpr int tDP = BQ;
+  static constexpr int tDQ = 2 * BQ;
+  static constexpr int tDV = D == 128 ? 256 : 320;
+  static constexpr int tDK = D == 128 ? 384 : 384;
+};
+
+struct Bars {
+  uint64_t kv_full;
+  uint64_t qdo_full[2], qdo_empty[2];
+  uint64_t s_full, dp_full, p_full, ds_full, dv_done, dsq_done, dq_full, dq_empty;
+  uint32_t tmem_base;
+};
+
+struct Step {
+  int h, q0, n_valid;  // q-head, first segment-relative query index, valid queries in the step
+};
+
+template <int D>
+__device__ __forceinline__ Step step_of(int n, int g, int grp, int qt_first, int nqt, int q_len) {
+  constexpr int BQ = Cfg<D>::BQ;
+  Step s;
+  const int hi = n / nqt, qt = qt_first + n % nqt;
+  s.h = g * grp + hi;
+  s.q0 = qt * BQ;
+  s.n_valid = min(BQ, q_len - s.q0);
+  return s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do, AttnArgs a,
+                    const float* __restrict__ lse, const float* __restrict__ Dbuf, float* __restrict__ dq_acc,
+                    void* __restrict__ dk_out, void* __restrict__ dv_out, int accumulate) {
+  using C = Cfg<D>;
+  constexpr int BQ = C::BQ;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
+  float* aux = reinterpret_cast<float*>(smem + C::kOffAux);  // lse2[2][BQ] then dd[2][BQ]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  const int g = blockIdx.x;
+  const int seg = a.tiles[2 * blockIdx.y], ktile = a.tiles[2 * blockIdx.y + 1];
+  const int grp = a.hq / a.hkv;
+  const int cu0 = a.cu[seg], q_len = a.cu[seg + 1] - cu0;
+  const int q_pos = a.q_pos[seg], k_len = a.k_len[seg], kst = a.k_start[seg];
+  const int kv0 = ktile * BN;
+  const int i_first = max(0, kv0 - q_pos);          // first query (segment-relative) that sees the tile
+  const int qt_first = i_first / BQ, qt_last = (q_len - 1) / BQ;
+  const int nqt = qt_last - qt_first + 1;
+  const int n_steps = grp * nqt;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->kv_full, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&bars->qdo_full[s], 33), mbar_init(&bars->qdo_empty[s], 1);
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->p_full, 128);
+    mbar_init(&bars->ds_full, 128);
+    mbar_init(&bars->dv_done, 1);
+    mbar_init(&bars->dsq_done, 1);
+    mbar_init(&bars->dq_full, 1);
+    mbar_init(&bars->dq_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 8) {
+    // ================= TMA producer (+ LSE / D rows of each step into smem)
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_do);
+      mbar_expect_tx(&bars->kv_full, 2 * C::kKVBytes);
+      for (int c = 0; c < C::kChunks; ++c) {
+        tma_load_2d(smem + C::kOffK + c * BN * 128, &tm_k, &bars->kv_full, g * D + c * 64, kst + kv0);
+        tma_load_2d(smem + C::kOffV + c * BN * 128, &tm_v, &bars->kv_full, g * D + c * 64, kst + kv0);
+      }
+    }
+    for (int n = 0; n < n_steps; ++n) {
+      const int st = n & 1;
+      const Step sp = step_of<D>(n, g, grp, qt_first, nqt, q_len);
+      mbar_wait(&bars->qdo_empty[st], ((n >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        mbar_expect_tx(&bars->qdo_full[st], 2 * C::kQBytes);
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(smem + C::kOffQ + st * C::kQBytes + c * BQ * 128, &tm_q, &bars->qdo_full[st],
+                      sp.h * D + c * 64, cu0 + sp.q0);
+          tma_load_2d(smem + C::kOffDO + st * C::kQBytes + c * BQ * 128, &tm_do, &bars->qdo_full[st],
+                      sp.h * D + c * 64, cu0 + sp.q0);
+        }
+      }
+      for (int i = lane; i < BQ; i += 32) {
+        const bool ok = i < sp.n_valid;
+        const size_t off = (size_t)sp.h * a.ld_lse + cu0 + sp.q0 + i;
+        aux[st * BQ + i] = ok ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid rows
+        aux[2 * BQ + st * BQ + i] = ok ? Dbuf[off] : 0.f;
+      }
+      __syncwarp();
+      mbar_arrive(&bars->qdo_full[st]);
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      const uint32_t sK = smem_u32(smem + C::kOffK), sV = smem_u32(smem + C::kOffV);
+      const uint32_t sQ = smem_u32(smem + C::kOffQ), sDO = smem_u32(smem + C::kOffDO);
+      const uint32_t sP = smem_u32(smem + C::kOffP), sDS = smem_u32(smem + C::kOffDS);
+      const uint32_t id_sdp = idesc_bf16_f32(BN, BQ, 0, 0);   // S^T = K Q^T, dP^T = V dO^T
+      const uint32_t id_kv = idesc_bf16_f32(BN, D, 0, 1);     // dV += P^T dO, dK += dS^T Q
+      // dQ^T = K^T dS^T (d = 128) or dQ = dS K (d = 64): both operands MN-major
+      const uint32_t id_dq = D == 128 ? idesc_bf16_f32(D, BQ, 1, 1) : idesc_bf16_f32(BQ, D, 1, 1);
+      // S^T / dP^T: A = K or V tile (K-major over d), B = Q or dO tile (K-major over d)
+      auto issue_t = [&](uint32_t a_base, uint32_t b_base, uint32_t tcol) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t ao = (k / 4) * (BN * 128) + (k % 4) * 32;
+          const uint32_t bo = (k / 4) * (BQ * 128) + (k % 4) * 32;
+          umma_f16(tmem + tcol, sdesc_sw128(a_base + ao, 16, 1024), sdesc_sw128(b_base + bo, 16, 1024), id_sdp,
+                   k > 0);
+        }
+      };
+      // dV / dK: A = P^T or dS^T [BN][BQ] (K-major over queries), B = dO or Q tile (MN-major over d)
+      auto issue_kv = [&](uint32_t a_base, uint32_t b_base, uint32_t tcol, bool acc) {
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k) {
+          const uint32_t ao = (k / 4) * (BN * 128) + (k % 4) * 32;
+          umma_f16(tmem + tcol, sdesc_sw128(a_base + ao, 16, 1024), sdesc_sw128(b_base + k * 2048, BQ * 128, 1024),
+                   id_kv, acc || k > 0);
+        }
+      };
+      auto issue_dq = [&]() {
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) {
+          if (D == 128)   // A = K^T (MN-major over d, chunks at BN*128), B = dS^T (MN-major over queries)
+            umma_f16(tmem + C::tDQ, sdesc_sw128(sK + k * 2048, BN * 128, 1024), sdesc_sw128(sDS + k * 2048, 0, 1024),
+                     id_dq, k > 0);
+          else            // A = dS (MN-major over queries, chunks at BN*128), B = K (MN-major over d)
+            umma_f16(tmem + C::tDQ, sdesc_sw128(sDS + k * 2048, BN * 128, 1024), sdesc_sw128(sK + k * 2048, 0, 1024),
+                     id_dq, k > 0);
+        }
+      };
+      mbar_wait(&bars->kv_full, 0);
+      mbar_wait(&bars->qdo_full[0], 0);
+      tc_fence_after();
+      issue_t(sK, sQ, C::tS);
+      umma_commit(&bars->s_full);
+      issue_t(sV, sDO, C::tDP);
+      umma_commit(&bars->dp_full);
+      for (int n = 0; n < n_steps; ++n) {
+        const int st = n & 1, st1 = (n + 1) & 1;
+        const bool more = n + 1 < n_steps;
+        mbar_wait(&bars->p_full, n & 1);
+        tc_fence_after();
+        issue_kv(sP, sDO + st * C::kQBytes, C::tDV, n > 0);
+        umma_commit(&bars->dv_done);
+        if (more) {
+          mbar_wait(&bars->qdo_full[st1], ((n + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_t(sK, sQ + st1 * C::kQBytes, C::tS);
+          umma_commit(&bars->s_full);
+        }
+        mbar_wait(&bars->ds_full, n & 1);
+        tc_fence_after();
+        issue_kv(sDS, sQ + st * C::kQBytes, C::tDK, n > 0);
+        mbar_wait(&bars->dq_empty, (n & 1) ^ 1);
+        tc_fence_after();
+        issue_dq();
+        umma_commit(&bars->dq_full);
+        umma_commit(&bars->dsq_done);
+        umma_commit(&bars->qdo_empty[st]);
+        if (more) {
+          issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
+          umma_commit(&bars->dp_full);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ================= compute warpgroup: thread = key row of the tile
+    const int j = warp * 32 + lane;
+    const int kvp = kv0 + j;                      // key position
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    const uint32_t sP = smem_u32(smem + C::kOffP), sDS = smem_u32(smem + C::kOffDS);
+    for (int n = 0; n < n_steps; ++n) {
+      const int st = n & 1;
+      const Step sp = step_of<D>(n, g, grp, qt_first, nqt, q_len);
+      const int qp_base = q_pos + sp.q0;          // position of the step's first query
+      mbar_wait(&bars->qdo_full[st], (n >> 1) & 1);
+      const float* lse2 = aux + st * BQ;
+      const float* dd = aux + 2 * BQ + st * BQ;
+      mbar_wait(&bars->s_full, n & 1);
+      tc_fence_after();
+      float p[BQ];
+#pragma unroll
+      for (int c = 0; c < BQ; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + C::tS + c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int qi = c + i;
+          const float e = ex2(fmaf(__uint_as_float(r[i]), sl2, -lse2[qi]));
+          p[qi] = (kvp <= qp_base + qi) ? e : 0.f;    // causal; invalid queries have lse2 = +inf
+        }
+      }
+      if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T smem free
+#pragma unroll
+      for (int c = 0; c < BQ; c += 8) {
+        const uint32_t addr = sP + (c / 64) * (BN * 128) + sw128_off(j, c % 64);
+        st_shared_v4(addr, pack_bf16(p[c], p[c + 1]), pack_bf16(p[c + 2], p[c + 3]), pack_bf16(p[c + 4], p[c + 5]),
+                     pack_bf16(p[c + 6], p[c + 7]));
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+      mbar_wait(&bars->dp_full, n & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BQ; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + C::tDP + c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) p[c + i] = p[c + i] * (__uint_as_float(r[i]) - dd[c + i]);
+      }
+      if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem free
+#pragma unroll
+      for (int c = 0; c < BQ; c += 8) {
+        const uint32_t addr = sDS + (c / 64) * (BN * 128) + sw128_off(j, c % 64);
+        st_shared_v4(addr, pack_bf16(p[c], p[c + 1]), pack_bf16(p[c + 2], p[c + 3]), pack_bf16(p[c + 4], p[c + 5]),
+                     pack_bf16(p[c + 6], p[c + 7]));
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->ds_full);
+    }
+    // ---- dK, dV epilogue
+    mbar_wait(&bars->dsq_done, (n_steps - 1) & 1);
+    tc_fence_after();
+    const bool valid = kvp < k_len;
+    const size_t row = (size_t)(kst + kvp) * a.hkv + g;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
+      const float mul = which == 0 ? a.scale : 1.f;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + tcol + c, r);
+        tmem_wait_ld();
+        if (!valid) continue;
+        if (accumulate) {
+          float* dst = reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D + c;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            red_add_v4(dst + i, __uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul,
+                       __uint_as_float(r[i + 2]) * mul, __uint_as_float(r[i + 3]) * mul);
+        } else {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(which == 0 ? dk_out : dv_out) + row * D + c;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul);
+            v.y = pack_bf16(__uint_as_float(r[i + 2]) * mul, __uint_as_float(r[i + 3]) * mul);
+            v.z = pack_bf16(__uint_as_float(r[i + 4]) * mul, __uint_as_float(r[i + 5]) * mul);
+            v.w = pack_bf16(__uint_as_float(r[i + 6]) * mul, __uint_as_float(r[i + 7]) * mul);
+            *reinterpret_cast<uint4*>(dst + i) = v;
+          }
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // ================= dQ reduction warpgroup
+    const int t = (warp - 4) * 32 + lane;        // TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+    for (int n = 0; n < n_steps; ++n) {
+      const Step sp = step_of<D>(n, g, grp, qt_first, nqt, q_len);
+      mbar_wait(&bars->dq_full, n & 1);
+      tc_fence_after();
+      if (D == 128) {
+        // dQ^T: lane = feature t, columns = queries of the step
+#pragma unroll
+        for (int c = 0; c < BQ; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_base + C::tDQ + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c + i < sp.n_valid)
+              atomicAdd(dq_acc + ((size_t)(cu0 + sp.q0 + c + i) * a.hq + sp.h) * D + t,
+                        __uint_as_float(r[i]) * a.scale);
+        }
+      } else {
+        // dQ: lane = query row t, columns = features
+        const bool ok = t < sp.n_valid;
+        float* dst = dq_acc + ((size_t)(cu0 + sp.q0 + t) * a.hq + sp.h) * D;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_base + C::tDQ + c, r);
+          tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              red_add_v4(dst + c + i, __uint_as_float(r[i]) * a.scale, __uint_as_float(r[i + 1]) * a.scale,
+                         __uint_as_float(r[i + 2]) * a.scale, __uint_as_float(r[i + 3]) * a.scale);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->dq_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+// D[h][r] = sum_c dO[r][h][c] * O[r][h][c] (bf16 in, fp32 out); zero the dQ accumulator rows.
+template <int D>
+__global__ void preprocess_kernel(int row_begin, int row_end, int hq, const __nv_bfloat16* __restrict__ o,
+                                  const __nv_bfloat16* __restrict__ dout, float* __restrict__ Dbuf, int ld,
+                                  float* __restrict__ dq_acc) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int64_t row = row_begin + gw / hq;
+  const int h = gw % hq;
+  if (row >= row_end) return;
+  const size_t base = ((size_t)row * hq + h) * D;
+  constexpr int E = D / 32;  // 2 or 4 elements per lane
+  float s = 0.f;
+  if (E == 4) {
+    const uint2 a = *reinterpret_cast<const uint2*>(o + base + lane * 4);
+    const uint2 b = *reinterpret_cast<const uint2*>(dout + base + lane * 4);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+    for (int i = 0; i < 2; ++i) {
+      float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
+      s += x.x * y.x + x.y * y.y;
+    }
+    *reinterpret_cast<float4*>(dq_acc + base + lane * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    const uint32_t a = *reinterpret_cast<const uint32_t*>(o + base + lane * 2);
+    const uint32_t b = *reinterpret_cast<const uint32_t*>(dout + base + lane * 2);
+    float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a));
+    float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b));
+    s = x.x * y.x + x.y * y.y;
+    *reinterpret_cast<float2*>(dq_acc + base + lane * 2) = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) Dbuf[(size_t)h * ld + row] = s;
+}
+
+__global__ void convert_dq_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, int64_t begin4,
+                                  int64_t end4) {
+  for (int64_t i = begin4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = acc[i];
+    uint2 o;
+    o.x = pack_bf16(v.x, v.y);
+    o.y = pack_bf16(v.z, v.w);
+    dq[i] = o;
+  }
+}
+
+}  // namespace bwd
 
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
                           const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
                           void* dv, int accumulate, float* Dbuf, float* dq_acc, int n_q_rows, int n_kv_rows,
                           cudaStream_t st) {
-  return fail(SKR_E_UNSUPPORTED, "bf16 backward not built yet");
+  if (d != 64 && d != 128) return fail(SKR_E_UNSUPPORTED, "bf16 backward supports d in {64,128}");
+  const int rows = row_end - row_begin;
+  if (rows > 0) {
+    const int64_t threads = (int64_t)rows * a.hq * 32;
+    const int blocks = (int)((threads + 255) / 256);
+    if (d == 128)
+      bwd::preprocess_kernel<128><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, (const __nv_bfloat16*)o,
+                                                          (const __nv_bfloat16*)dout, Dbuf, a.ld_lse, dq_acc);
+    else
+      bwd::preprocess_kernel<64><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, (const __nv_bfloat16*)o,
+                                                         (const __nv_bfloat16*)dout, Dbuf, a.ld_lse, dq_acc);
+    if (skr_status e = launch_status("attn bwd preprocess")) return e;
+  }
+  if (a.n_tiles > 0) {
+    CUtensorMap tq, tk, tv, tdo;
+    const uint64_t qcols = (uint64_t)a.hq * d, kcols = (uint64_t)a.hkv * d;
+    const uint32_t bq = d == 128 ? 64 : 128;
+    if (!make_tmap_2d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, bq, 64, true) ||
+        !make_tmap_2d(&tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, bq, 64, true) ||
+        !make_tmap_2d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true) ||
+        !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true))
+      return fail(SKR_E_CUDA, "attn bwd: tensor map encode failed");
+    dim3 grid(a.hkv, a.n_tiles);
+    if (d == 128) {
+      constexpr int smem = bwd::Cfg<128>::kSmem;
+      cudaFuncSetAttribute(bwd::attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      bwd::attn_bwd_kernel<128><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, a, lse, Dbuf, dq_acc, dk, dv,
+                                                                   accumulate);
+    } else {
+      constexpr int smem = bwd::Cfg<64>::kSmem;
+      cudaFuncSetAttribute(bwd::attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      bwd::attn_bwd_kernel<64><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, a, lse, Dbuf, dq_acc, dk, dv,
+                                                                  accumulate);
+    }
+    if (skr_status e = launch_status("attn_bwd_kernel")) return e;
+  }
+  if (rows > 0) {
+    const int64_t b4 = (int64_t)row_begin * a.hq * d / 4, e4 = (int64_t)row_end * a.hq * d / 4;
+    const int blocks = (int)std::min<int64_t>((e4 - b4 + 255) / 256, 148 * 16);
+    bwd::convert_dq_kernel<<<blocks, 256, 0, st>>>((const float4*)dq_acc, (uint2*)dq, b4, e4);
+    if (skr_status e = launch_status("attn bwd dq convert")) return e;
+  }
+  return SKR_OK;
 }
 
 }  // namespace skr

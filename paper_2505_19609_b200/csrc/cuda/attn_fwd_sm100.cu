@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars->pv_done[s], (j - 1) & 1);
           tc_fence_after();
         }
-        if (m_new > m_ref + kRescaleThreshold || j == 0) {
+        // tcgen05.ld/st are warp-collective: the rescale decision is made per warp (every lane of
+        // the warp moves its reference max to its own m_new; alpha == 1 where nothing changed)
+        if (__any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0) {
           const float alpha = j == 0 ? 0.f : ex2(m_ref - m_new);
           if (j > 0) {
 #pragma unroll

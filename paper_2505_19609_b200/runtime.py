@@ -1,0 +1,223 @@
+"""CP-rank runtime for one DACP micro-batch: buffers, device tables and the launch order of rows
+a5-a9 (SURVEY.md §3 stacks 2-3), all through the C-ABI (`skrull.py`).
+
+Forward (Eq. 2, P:156 executed literally):
+  main : pack Q,K,V (a5)                                          -> ev_packed
+  side : wait ev_packed; all-gather K,V distributed prefix (a6);
+         reorder rank-major -> natural distributed order           -> ev_kv
+  main : attention fwd over LOCAL segments (overlaps the exchange)
+  main : wait ev_kv; attention fwd over DISTRIBUTED chunks
+Backward (mirror, reading R24):
+  main : pack dO; attention bwd over DISTRIBUTED chunks (fp32 dK/dV partials, natural order) -> ev_dkv
+  side : wait ev_dkv; permute natural -> rank-major (a9); reduce-scatter; cast into the packed
+         dK/dV distributed prefix                                                          -> ev_rs
+  main : attention bwd over LOCAL segments (overlaps the exchange); wait ev_rs
+With N = 1 (or no distributed sequence) no collective is issued (T_comm(0) = 0, R26).
+
+Each phase is a method so a test can drive N ranks on one GPU with a loopback exchange
+(`loopback_step`); `forward` / `backward` are the production composition over a `Comm`.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import skrull as sk
+
+
+class RankStep:
+    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda"):
+        self.shape, self.cp, self.rank = shape, cp, rank
+        self.dev = device
+        hq, hkv, d = shape.hq, shape.hkv, shape.d
+        self.dt = torch.bfloat16 if shape.dtype == sk.SKR_BF16 else torch.float32
+        pr = sk.skr_pack_rank(mb_lens, assign, cp, rank)
+        self.pr = pr
+        self.rows = pr["n_rows"]
+        self.dist_rows = pr["dist_rows"]
+        self.P = pr["pad_rows_P"]
+        self.nat_rows = pr["natural_rows"]
+        self.n_chunks = pr["n_chunks"]
+        nd, ns = pr["n_dist_seg"], pr["n_seg"]
+        cu, qp, ks, kl = pr["cu_seqlens_q"], pr["q_pos"], pr["k_start"], pr["k_len"]
+        self.has_dist = self.nat_rows > 0
+        self.src_row = torch.as_tensor(pr["src_row"]).to(device)
+        # segment classes: distributed chunks [0, nd), locals [nd, ns)
+        self.dist_f = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "fwd", device)
+        self.dist_b = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "bwd", device)
+        self.loc_f = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "fwd", device)
+        self.loc_b = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "bwd", device)
+        if self.has_dist:
+            self.chunks = torch.as_tensor(sk.skr_pack_chunks(mb_lens, assign, cp).reshape(-1)).to(device)
+        # packed buffers (>= P rows so the all-gather send prefix is always in bounds)
+        R = max(self.rows, self.P, 1)
+        e = lambda *s, dt=None: torch.empty(*s, device=device, dtype=dt or self.dt)  # noqa: E731
+        self.q, self.o, self.do, self.dq = (e(R, hq, d) for _ in range(4))
+        self.k, self.v, self.dk, self.dv = (e(R, hkv, d) for _ in range(4))
+        self.lse = torch.empty(hq, R, device=device, dtype=torch.float32)
+        self.ws = torch.empty(sk.skr_attn_bwd_ws_bytes(shape, R) // 4 + 64, device=device, dtype=torch.float32)
+        if self.has_dist:
+            N, P, nat = cp, self.P, max(self.nat_rows, 1)
+            self.k_gath, self.v_gath = e(N * P, hkv, d), e(N * P, hkv, d)
+            self.k_nat, self.v_nat = e(nat, hkv, d), e(nat, hkv, d)
+            f32 = torch.float32
+            self.dk_nat, self.dv_nat = e(nat, hkv, d, dt=f32), e(nat, hkv, d, dt=f32)
+            self.dk_rm, self.dv_rm = e(N * P, hkv, d, dt=f32), e(N * P, hkv, d, dt=f32)
+            self.dk_red, self.dv_red = e(P, hkv, d, dt=f32), e(P, hkv, d, dt=f32)
+
+    def launches_per_step(self) -> int:
+        """Kernels of this library launched by one forward + backward of this micro-batch."""
+        n = 0
+        if self.rows:
+            n += 4                                            # pack Q, K, V, dO
+        loc_rows = self.loc_b.row_end - self.loc_b.row_begin
+        n += (self.loc_f.n_tiles > 0) + (self.loc_b.n_tiles > 0) + 2 * (loc_rows > 0)
+        if self.has_dist:
+            dist_rows = self.dist_b.row_end - self.dist_b.row_begin
+            n += 2 + (self.dist_f.n_tiles > 0)                # reorder K, V; fwd
+            n += (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)
+            n += 2 + 2 * (self.dist_rows > 0)                 # scatter dK, dV; cast dK, dV
+        return n
+
+    # ------------------------------------------------------------------ phases
+    def pack_qkv(self, q_src, k_src, v_src, stream=None):
+        if self.rows:
+            sk.skr_pack_rows(q_src, self.src_row, self.q[:self.rows], stream)
+            sk.skr_pack_rows(k_src, self.src_row, self.k[:self.rows], stream)
+            sk.skr_pack_rows(v_src, self.src_row, self.v[:self.rows], stream)
+
+    def pack_do(self, do_src, stream=None):
+        if self.rows:
+            sk.skr_pack_rows(do_src, self.src_row, self.do[:self.rows], stream)
+
+    def kv_send(self):
+        return self.k[:self.P], self.v[:self.P]
+
+    def kv_reorder(self, stream=None):
+        sk.skr_gather_chunks(self.k_gath, self.chunks, self.n_chunks, self.k_nat, stream)
+        sk.skr_gather_chunks(self.v_gath, self.chunks, self.n_chunks, self.v_nat, stream)
+
+    def fwd_local(self, stream=None):
+        sk.skr_attn_fwd(self.shape, self.loc_f, self.q, self.k, self.v, self.o, self.lse, stream)
+
+    def fwd_dist(self, stream=None):
+        sk.skr_attn_fwd(self.shape, self.dist_f, self.q, self.k_nat, self.v_nat, self.o, self.lse, stream)
+
+    def bwd_dist(self, stream=None):
+        self.dk_nat.zero_()
+        self.dv_nat.zero_()
+        sk.skr_attn_bwd(self.shape, self.dist_b, self.q, self.k_nat, self.v_nat, self.o, self.do, self.lse, self.dq,
+                        self.dk_nat, self.dv_nat, 1, self.ws, stream)
+
+    def grad_scatter(self, stream=None):
+        sk.skr_scatter_chunks(self.dk_nat, self.chunks, self.n_chunks, self.P, self.cp, self.dk_rm, stream)
+        sk.skr_scatter_chunks(self.dv_nat, self.chunks, self.n_chunks, self.P, self.cp, self.dv_rm, stream)
+
+    def grad_cast(self, stream=None):
+        n = self.dist_rows
+        if n:
+            if self.dt == torch.float32:
+                self.dk[:n].copy_(self.dk_red[:n])
+                self.dv[:n].copy_(self.dv_red[:n])
+            else:
+                sk.skr_cast_f32_bf16(self.dk_red[:n], self.dk[:n], stream)
+                sk.skr_cast_f32_bf16(self.dv_red[:n], self.dv[:n], stream)
+
+    def bwd_local(self, stream=None):
+        sk.skr_attn_bwd(self.shape, self.loc_b, self.q, self.k, self.v, self.o, self.do, self.lse, self.dq, self.dk,
+                        self.dv, 0, self.ws, stream)
+
+    # ------------------------------------------------------------------ production composition
+    def forward(self, q_src, k_src, v_src, comm=None, side=None):
+        main = torch.cuda.current_stream()
+        self.pack_qkv(q_src, k_src, v_src)
+        if self.has_dist:
+            ev_packed = torch.cuda.Event()
+            ev_packed.record(main)
+            side.wait_event(ev_packed)
+            with torch.cuda.stream(side):
+                ks, vs = self.kv_send()
+                comm.all_gather(ks, self.k_gath, side)
+                comm.all_gather(vs, self.v_gath, side)
+                self.kv_reorder(side)
+                ev_kv = torch.cuda.Event()
+                ev_kv.record(side)
+        self.fwd_local()
+        if self.has_dist:
+            main.wait_event(ev_kv)
+            self.fwd_dist()
+
+    def backward(self, do_src, comm=None, side=None):
+        main = torch.cuda.current_stream()
+        self.pack_do(do_src)
+        if self.has_dist:
+            self.bwd_dist()
+            ev_dkv = torch.cuda.Event()
+            ev_dkv.record(main)
+            side.wait_event(ev_dkv)
+            with torch.cuda.stream(side):
+                self.grad_scatter(side)
+                comm.reduce_scatter_f32(self.dk_rm, self.dk_red, side)
+                comm.reduce_scatter_f32(self.dv_rm, self.dv_red, side)
+                self.grad_cast(side)
+                ev_rs = torch.cuda.Event()
+                ev_rs.record(side)
+        self.bwd_local()
+        if self.has_dist:
+            main.wait_event(ev_rs)
+
+
+def loopback_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
+    """Debug aid: run N RankSteps of one micro-batch on ONE GPU, the all-gather and
+    reduce-scatter replaced by device copies. Same kernels and tables as production."""
+    N = len(ranks)
+    for r, x in enumerate(ranks):
+        x.pack_qkv(q_srcs[r], k_srcs[r], v_srcs[r])
+        x.pack_do(do_srcs[r])
+    if ranks[0].has_dist:
+        P = ranks[0].P
+        for x in ranks:
+            for j, y in enumerate(ranks):
+                ks, vs = y.kv_send()
+                x.k_gath[j * P:(j + 1) * P].copy_(ks)
+                x.v_gath[j * P:(j + 1) * P].copy_(vs)
+            x.kv_reorder()
+    for x in ranks:
+        x.fwd_local()
+        if x.has_dist:
+            x.fwd_dist()
+    if ranks[0].has_dist:
+        for x in ranks:
+            x.bwd_dist()
+            x.grad_scatter()
+        P = ranks[0].P
+        for j, x in enumerate(ranks):
+            x.dk_red.copy_(sum(y.dk_rm[j * P:(j + 1) * P] for y in ranks))
+            x.dv_red.copy_(sum(y.dv_rm[j * P:(j + 1) * P] for y in ranks))
+            x.grad_cast()
+    for x in ranks:
+        x.bwd_local()
+    del N
+    return ranks
+
+
+def rank_natural_rows(lens, assign, cp, rank):
+    """Rows of this rank's rank-natural source buffer as (seq, lo, hi) position ranges, in order
+    (input order; a distributed sequence contributes chunk min(j, 2N-1-j) then max)."""
+    out = []
+    for k, S in enumerate(lens):
+        S = int(S)
+        if assign[k] == rank:
+            out.append((k, 0, S))
+        elif assign[k] == -1:
+            for c in sorted((rank, 2 * cp - 1 - rank)):
+                out.append((k, c * S // (2 * cp), (c + 1) * S // (2 * cp)))
+    return out
+
+
+def gather_rank_natural(per_seq, lens, assign, cp, rank, key):
+    """Concatenate per-sequence arrays (numpy [S, H, d]) into this rank's rank-natural buffer."""
+    parts = [per_seq[k][key][lo:hi] for k, lo, hi in rank_natural_rows(lens, assign, cp, rank)]
+    if not parts:
+        return np.zeros((0,) + per_seq[0][key].shape[1:], np.float32)
+    return np.concatenate(parts, axis=0)

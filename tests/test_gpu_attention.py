@@ -28,7 +28,7 @@ def _run_fwd(sk, shape, pk, dtype):
 
 def _check_fwd(pk, O, LSE, fp32):
     r = 0
-    for (s, lo, hi), in zip(((x,) for x in pk.segs)):
+    for s, lo, hi in pk.segs:
         Oref, Lref, *_ = oracle_seq(pk.inputs[s], bwd=False)
         n = hi - lo
         ok, err, bound = tol_ok(O[r:r + n], Oref[lo:hi], fp32)
@@ -97,3 +97,103 @@ def test_fwd_fp32_local():
     shape = sk.attn_shape(2, 2, 64, sk.SKR_FP32)
     O, L = _run_fwd(sk, shape, pk, torch.float32)
     _check_fwd(pk, O, L, fp32=True)
+
+
+# ----------------------------------------------------------------------------- backward
+
+
+def _run_bwd(sk, shape, pk, kv_accumulate=False):
+    """fwd + bwd of one segment class; returns O, LSE, dQ, dK, dV (float numpy)."""
+    segs_f = sk.make_segs(shape, pk.cu, pk.q_pos, pk.k_start, pk.k_len, "fwd")
+    segs_b = sk.make_segs(shape, pk.cu, pk.q_pos, pk.k_start, pk.k_len, "bwd")
+    o = torch.zeros_like(pk.q)
+    lse = torch.zeros(shape.hq, max(pk.rows, 1), device="cuda", dtype=torch.float32)
+    sk.skr_attn_fwd(shape, segs_f, pk.q, pk.k, pk.v, o, lse)
+    dq = torch.full_like(pk.q, float("nan"))
+    if kv_accumulate:
+        dk = torch.zeros(pk.k.shape, device="cuda", dtype=torch.float32)
+        dv = torch.zeros_like(dk)
+    else:
+        dk = torch.zeros_like(pk.k)
+        dv = torch.zeros_like(pk.v)
+    ws = torch.empty(sk.skr_attn_bwd_ws_bytes(shape, pk.rows) // 4 + 1, device="cuda", dtype=torch.float32)
+    sk.skr_attn_bwd(shape, segs_b, pk.q, pk.k, pk.v, o, pk.do, lse, dq, dk, dv, int(kv_accumulate), ws)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    return f(o), f(lse), f(dq), f(dk), f(dv)
+
+
+def _check_bwd_local(pk, dQ, dK, dV, fp32):
+    r = 0
+    for s, lo, hi in pk.segs:
+        assert lo == 0
+        _, _, rq, rk, rv = oracle_seq(pk.inputs[s])
+        n = hi - lo
+        for name, got, ref in (("dQ", dQ[r:r + n], rq), ("dK", dK[r:r + n], rk), ("dV", dV[r:r + n], rv)):
+            ok, err, bound = tol_ok(got, ref, fp32)
+            assert ok, f"{name} seq {s} (len {n}): err {err} > {bound}"
+        r += n
+
+
+@pytest.mark.parametrize("hq,hkv,d", SHAPES)
+def test_bwd_bf16_local_ragged(hq, hkv, d):
+    sk = _sk()
+    lens = [1, 17, 128, 129, 300, 777, 0, 256, 1100]
+    inputs = make_inputs(lens, hq, hkv, d, seed=5)
+    pk = local_pack(inputs, torch.bfloat16)
+    shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16)
+    O, L, dQ, dK, dV = _run_bwd(sk, shape, pk)
+    _check_fwd(pk, O, L, fp32=False)
+    _check_bwd_local(pk, dQ, dK, dV, fp32=False)
+
+
+def test_bwd_fp32_local():
+    sk = _sk()
+    lens = [1, 33, 64, 90, 200, 300]
+    inputs = make_inputs(lens, 2, 1, 64, seed=6, bf16=False)
+    pk = local_pack(inputs, torch.float32)
+    shape = sk.attn_shape(2, 1, 64, sk.SKR_FP32)
+    O, L, dQ, dK, dV = _run_bwd(sk, shape, pk)
+    _check_fwd(pk, O, L, fp32=True)
+    _check_bwd_local(pk, dQ, dK, dV, fp32=True)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_bwd_distributed_chunks_sum_to_unsharded(dtype, N):
+    # every rank's zigzag chunks (R20) against the natural K/V buffer; per-rank fp32 dK/dV
+    # partials summed over ranks (the reduce-scatter's job) equal the unsharded gradients.
+    sk = _sk()
+    hq, hkv, d = 8, 2, 64 if dtype == "fp32" else 128
+    lens = [5, 700, 1333]
+    bf = dtype == "bf16"
+    inputs = make_inputs(lens, hq, hkv, d, seed=7, bf16=bf)
+    tdt = torch.bfloat16 if bf else torch.float32
+    shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16 if bf else sk.SKR_FP32)
+    base, acc = {}, 0
+    for s, S in enumerate(lens):
+        base[s] = acc
+        acc += S
+    dk_sum = np.zeros((acc, hkv, d))
+    dv_sum = np.zeros((acc, hkv, d))
+    refs = [oracle_seq(x) for x in inputs]
+    for j in range(N):
+        segs = []
+        for s, S in enumerate(lens):
+            for c in (j, 2 * N - 1 - j):
+                segs.append((s, c * S // (2 * N), (c + 1) * S // (2 * N)))
+        pk = Packed(inputs, segs, base, list(range(len(lens))), tdt)
+        O, L, dQ, dK, dV = _run_bwd(sk, shape, pk, kv_accumulate=True)
+        _check_fwd(pk, O, L, fp32=not bf)
+        r = 0
+        for s, lo, hi in segs:
+            ok, err, bound = tol_ok(dQ[r:r + hi - lo], refs[s][2][lo:hi], not bf)
+            assert ok, f"dQ rank {j} seq {s} [{lo},{hi}): {err} > {bound}"
+            r += hi - lo
+        dk_sum += dK[:acc]
+        dv_sum += dV[:acc]
+    for s, S in enumerate(lens):
+        for name, got, ref in (("dK", dk_sum[base[s]:base[s] + S], refs[s][3]),
+                               ("dV", dv_sum[base[s]:base[s] + S], refs[s][4])):
+            ok, err, bound = tol_ok(got, ref, not bf)
+            assert ok, f"{name} seq {s}: {err} > {bound}"

@@ -1,0 +1,92 @@
+"""GPU: the CP runtime (pack -> K/V exchange -> fwd local/dist -> bwd dist/local -> dK/dV exchange)
+for N ranks driven on ONE GPU with a loopback exchange (SURVEY §4 debug aid), checked against the
+unsharded fp64 oracle: sharded == unsharded for every sequence, every output.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.attention import attn_bwd, attn_fwd  # noqa: E402
+from oracle.schedule import plan as oracle_plan  # noqa: E402
+from oracle.cost_model import Model  # noqa: E402
+from tests.attn_harness import make_inputs, tol_ok  # noqa: E402
+
+
+def _run(lens, hq, hkv, d, N, C, bf16, seed):
+    from paper_2505_19609_b200 import skrull as sk
+    from paper_2505_19609_b200.runtime import RankStep, gather_rank_natural, loopback_step
+    shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16 if bf16 else sk.SKR_FP32)
+    p = sk.skr_plan(lens, C, N, 1, hq * d, hkv * d)
+    ref = oracle_plan(list(lens), C, N, 1, Model(hq * d, hkv * d))
+    assert list(p["assign"]) == ref.assign                       # bit-exact plan
+    inputs = make_inputs(lens, hq, hkv, d, seed=seed, bf16=bf16)
+    tdt = torch.bfloat16 if bf16 else torch.float32
+    outs = {k: [np.full((int(S),) + x[k].shape[1:], np.nan) for S, x in zip(lens, inputs)]
+            for k in ("o", "dq", "dk", "dv")}
+    lse = [np.full((hq, int(S)), np.nan) for S in lens]
+    n_dist = 0
+    for j in range(int(p["n_mb_per_dp"][0])):
+        idx = np.nonzero(p["mb_of_seq"] == j)[0]
+        ml, ma = np.asarray(lens)[idx], p["assign"][idx]
+        n_dist += int((ma == -1).sum())
+        mb_inputs = [inputs[i] for i in idx]
+        ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
+        srcs = {k: [torch.from_numpy(gather_rank_natural(mb_inputs, ml, ma, N, r, k)).to("cuda", tdt)
+                    for r in range(N)] for k in ("q", "k", "v", "do")}
+        loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+        torch.cuda.synchronize()
+        for r, rs in enumerate(ranks):
+            pr = rs.pr
+            f = lambda t: t.float().cpu().numpy()  # noqa: E731
+            o, dq, dk, dv, L = f(rs.o), f(rs.dq), f(rs.dk), f(rs.dv), f(rs.lse)
+            for i in range(pr["n_seg"]):
+                a, b = pr["cu_seqlens_q"][i], pr["cu_seqlens_q"][i + 1]
+                s = idx[pr["seg_seq"][i]]
+                lo = pr["q_pos"][i]
+                for key, arr in (("o", o), ("dq", dq), ("dk", dk), ("dv", dv)):
+                    outs[key][s][lo:lo + b - a] = arr[a:b]
+                lse[s][:, lo:lo + b - a] = L[:, a:b]
+    for s, x in enumerate(inputs):
+        O, Lr = attn_fwd(x["q"], x["k"], x["v"])
+        dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
+        for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
+            got = outs[key][s]
+            assert not np.isnan(got).any(), f"{key} seq {s}: rows not covered"
+            ok, err, bound = tol_ok(got, ref, not bf16)
+            assert ok, f"{key} seq {s} (len {lens[s]}, N={N}): err {err} > {bound}"
+        assert np.abs(lse[s] - Lr).max() <= (2e-2 if bf16 else 1e-5 * max(1, np.abs(Lr).max()))
+    return n_dist, p
+
+
+def test_toy_c1_fp32_cp2():
+    # BASELINE configs[0]: toy 8 sequences, 2 heads, d=64, fp32, CP=2 plan (C=600): 3 distributed
+    n_dist, p = _run([17, 33, 64, 90, 128, 200, 256, 300], 2, 2, 64, 2, 600, False, 0)
+    assert n_dist == 3 and p["n_rollbacks"] == 2
+
+
+def test_toy_c1_gqa_fp32_cp2():
+    _run([17, 33, 64, 90, 128, 200, 256, 300], 2, 1, 64, 2, 600, False, 1)
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_bf16_cp_mixed(N):
+    # long + short mix with C below the longest sequence (R33): the long ones are sharded
+    lens = [1500, 37, 300, 129, 1, 600, 64, 2000, 250]
+    C = 1600 if N == 2 else 900
+    n_dist, _ = _run(lens, 8, 2, 128, N, C, True, 2)
+    assert n_dist >= 1
+
+
+def test_bf16_cp_d64_rollback_cascade():
+    # tiny sequences rolled back into distributed status: chunks of 0-2 tokens (S < 2N)
+    lens = [3, 5, 2, 700, 800, 1, 7]
+    n_dist, p = _run(lens, 14, 2, 64, 4, 400, True, 3)
+    assert n_dist >= 2
+
+
+def test_n1_all_local():
+    lens = [1, 17, 300, 129, 1024]
+    n_dist, p = _run(lens, 14, 2, 64, 1, 4096, True, 4)
+    assert n_dist == 0
