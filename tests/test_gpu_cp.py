@@ -23,7 +23,8 @@ def _run(lens, hq, hkv, d, N, C, bf16, seed):
     assert list(p["assign"]) == ref.assign                       # bit-exact plan
     inputs = make_inputs(lens, hq, hkv, d, seed=seed, bf16=bf16)
     tdt = torch.bfloat16 if bf16 else torch.float32
-    outs = {k: [np.full((int(S),) + x[k].shape[1:], np.nan) for S, x in zip(lens, inputs)]
+    src_key = {"o": "q", "dq": "q", "dk": "k", "dv": "k"}
+    outs = {k: [np.full((int(S),) + x[src_key[k]].shape[1:], np.nan) for S, x in zip(lens, inputs)]
             for k in ("o", "dq", "dk", "dv")}
     lse = [np.full((hq, int(S)), np.nan) for S in lens]
     n_dist = 0
