@@ -11,9 +11,10 @@
 //            dQ^T = K^T dS^T (M = d): thread = feature, reductions coalesced along d.
 //   d =  64: query step BQ = 128. TMEM: S^T[0,128) dP^T[128,256) dQ[256,320) dV[320,384) dK[384,448)
 //            dQ = dS K (M = query rows).
-// Warp roles (320 threads): warps 0-3 compute (thread = key row: P^T, dS^T from TMEM -> bf16
-// swizzled smem), warps 4-7 dQ reduction (TMEM -> fp32 red.global into the dQ accumulator),
-// warp 8 TMA producer (K, V once; Q/dO ring of 2 + LSE/D rows), warp 9 MMA issuer.
+// Warp roles (448 threads): warps 0-7 two compute warpgroups (thread = key row; warpgroup w owns
+// query columns [w*BQ/2, (w+1)*BQ/2): P^T, dS^T from TMEM -> bf16 swizzled smem), warps 8-11 dQ
+// (TMEM -> scaled fp32 SW128 smem tile -> one TMA bulk reduce-add per 32-column box into the fp32
+// dQ accumulator), warp 12 TMA producer (K, V once; Q/dO ring of 2 + LSE/D rows), warp 13 MMA.
 // MMA order per step n:  S(n) dP(n) | P(n) -> dV(n) S(n+1) | dS(n) -> dK(n) dQ(n) dP(n+1)
 // so the tensor core works on one half of the step while the compute warpgroup does the other.
 #include "attn_common.cuh"
@@ -25,22 +26,26 @@ namespace skr {
 namespace bwd {
 
 constexpr int BN = 128;  // key tile
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;
+constexpr int kComputeThreads = 256;
 
 template <int D>
 struct Cfg {
-  static constexpr int BQ = D == 128 ? 64 : 128;
+  static constexpr int BQ = D == 128 ? 64 : 128;         // query step
+  static constexpr int H = BQ / 2;                       // columns per compute warpgroup
   static constexpr int kChunks = D / 64;
   static constexpr int kKVBytes = BN * D * 2;
   static constexpr int kQBytes = BQ * D * 2;
   static constexpr int kPBytes = BN * BQ * 2;
+  static constexpr int kDQBytes = BQ * D * 4;            // fp32 dQ tile, SW128 boxes of 32 columns
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kKVBytes;
   static constexpr int kOffQ = kOffV + kKVBytes;          // [2] stages
   static constexpr int kOffDO = kOffQ + 2 * kQBytes;      // [2] stages
   static constexpr int kOffP = kOffDO + 2 * kQBytes;
   static constexpr int kOffDS = kOffP + kPBytes;
-  static constexpr int kOffAux = kOffDS + kPBytes;        // lse2[2][BQ], dd[2][BQ] fp32
+  static constexpr int kOffDQ = kOffDS + kPBytes;
+  static constexpr int kOffAux = kOffDQ + kDQBytes;       // lse2[2][BQ], dd[2][BQ] fp32
   static constexpr int kOffBar = kOffAux + 4 * BQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   // TMEM columns
@@ -48,7 +53,7 @@ struct Cfg {
   static constexpr int tDP = BQ;
   static constexpr int tDQ = 2 * BQ;
   static constexpr int tDV = D == 128 ? 256 : 320;
-  static constexpr int tDK = D == 128 ? 384 : 384;
+  static constexpr int tDK = 384;
 };
 
 struct Bars {
@@ -58,29 +63,24 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-struct Step {
-  int h, q0, n_valid;  // q-head, first segment-relative query index, valid queries in the step
+// Steps n = (q-head of the group, query tile); iterated incrementally by every role.
+struct StepIter {
+  int hi, qt, qt_first, qt_last;
+  __device__ StepIter(int first, int last) : hi(0), qt(first), qt_first(first), qt_last(last) {}
+  __device__ void next() {
+    if (++qt > qt_last) qt = qt_first, ++hi;
+  }
 };
-
-template <int D>
-__device__ __forceinline__ Step step_of(int n, int g, int grp, int qt_first, int nqt, int q_len) {
-  constexpr int BQ = Cfg<D>::BQ;
-  Step s;
-  const int hi = n / nqt, qt = qt_first + n % nqt;
-  s.h = g * grp + hi;
-  s.q0 = qt * BQ;
-  s.n_valid = min(BQ, q_len - s.q0);
-  return s;
-}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do, AttnArgs a,
-                    const float* __restrict__ lse, const float* __restrict__ Dbuf, float* __restrict__ dq_acc,
-                    void* __restrict__ dk_out, void* __restrict__ dv_out, int accumulate) {
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_dq, AttnArgs a, const float* __restrict__ lse,
+                    const float* __restrict__ Dbuf, void* __restrict__ dk_out, void* __restrict__ dv_out,
+                    int accumulate) {
   using C = Cfg<D>;
-  constexpr int BQ = C::BQ;
+  constexpr int BQ = C::BQ, H = C::H;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
@@ -95,64 +95,65 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kv0 = ktile * BN;
   const int i_first = max(0, kv0 - q_pos);          // first query (segment-relative) that sees the tile
   const int qt_first = i_first / BQ, qt_last = (q_len - 1) / BQ;
-  const int nqt = qt_last - qt_first + 1;
-  const int n_steps = grp * nqt;
+  const int n_steps = grp * (qt_last - qt_first + 1);
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
     for (int s = 0; s < 2; ++s) mbar_init(&bars->qdo_full[s], 33), mbar_init(&bars->qdo_empty[s], 1);
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
-    mbar_init(&bars->p_full, 128);
-    mbar_init(&bars->ds_full, 128);
+    mbar_init(&bars->p_full, kComputeThreads);
+    mbar_init(&bars->ds_full, kComputeThreads);
     mbar_init(&bars->dv_done, 1);
     mbar_init(&bars->dsq_done, 1);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_empty, 128);
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp == 8) {
+  if (warp == 12) {
     // ================= TMA producer (+ LSE / D rows of each step into smem)
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_do);
+      tma_prefetch_desc(&tm_dq);
       mbar_expect_tx(&bars->kv_full, 2 * C::kKVBytes);
       for (int c = 0; c < C::kChunks; ++c) {
         tma_load_2d(smem + C::kOffK + c * BN * 128, &tm_k, &bars->kv_full, g * D + c * 64, kst + kv0);
         tma_load_2d(smem + C::kOffV + c * BN * 128, &tm_v, &bars->kv_full, g * D + c * 64, kst + kv0);
       }
     }
-    for (int n = 0; n < n_steps; ++n) {
+    StepIter it(qt_first, qt_last);
+    for (int n = 0; n < n_steps; ++n, it.next()) {
       const int st = n & 1;
-      const Step sp = step_of<D>(n, g, grp, qt_first, nqt, q_len);
+      const int h = g * grp + it.hi, q0 = it.qt * BQ, nv = min(BQ, q_len - q0);
       mbar_wait(&bars->qdo_empty[st], ((n >> 1) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&bars->qdo_full[st], 2 * C::kQBytes);
         for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_2d(smem + C::kOffQ + st * C::kQBytes + c * BQ * 128, &tm_q, &bars->qdo_full[st],
-                      sp.h * D + c * 64, cu0 + sp.q0);
+          tma_load_2d(smem + C::kOffQ + st * C::kQBytes + c * BQ * 128, &tm_q, &bars->qdo_full[st], h * D + c * 64,
+                      cu0 + q0);
           tma_load_2d(smem + C::kOffDO + st * C::kQBytes + c * BQ * 128, &tm_do, &bars->qdo_full[st],
-                      sp.h * D + c * 64, cu0 + sp.q0);
+                      h * D + c * 64, cu0 + q0);
         }
       }
       for (int i = lane; i < BQ; i += 32) {
-        const bool ok = i < sp.n_valid;
-        const size_t off = (size_t)sp.h * a.ld_lse + cu0 + sp.q0 + i;
-        aux[st * BQ + i] = ok ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid rows
+        const bool ok = i < nv;
+        const size_t off = (size_t)h * a.ld_lse + cu0 + q0 + i;
+        aux[st * BQ + i] = ok ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
         aux[2 * BQ + st * BQ + i] = ok ? Dbuf[off] : 0.f;
       }
       __syncwarp();
       mbar_arrive(&bars->qdo_full[st]);
     }
-  } else if (warp == 9) {
+  } else if (warp == 13) {
     // ================= MMA issuer
     if (lane == 0) {
       const uint32_t sK = smem_u32(smem + C::kOffK), sV = smem_u32(smem + C::kOffV);
@@ -162,7 +163,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_kv = idesc_bf16_f32(BN, D, 0, 1);     // dV += P^T dO, dK += dS^T Q
       // dQ^T = K^T dS^T (d = 128) or dQ = dS K (d = 64): both operands MN-major
       const uint32_t id_dq = D == 128 ? idesc_bf16_f32(D, BQ, 1, 1) : idesc_bf16_f32(BQ, D, 1, 1);
-      // S^T / dP^T: A = K or V tile (K-major over d), B = Q or dO tile (K-major over d)
       auto issue_t = [&](uint32_t a_base, uint32_t b_base, uint32_t tcol) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                    k > 0);
         }
       };
-      // dV / dK: A = P^T or dS^T [BN][BQ] (K-major over queries), B = dO or Q tile (MN-major over d)
       auto issue_kv = [&](uint32_t a_base, uint32_t b_base, uint32_t tcol, bool acc) {
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k) {
@@ -184,10 +183,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_dq = [&]() {
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k) {
-          if (D == 128)   // A = K^T (MN-major over d, chunks at BN*128), B = dS^T (MN-major over queries)
+          if (D == 128)
             umma_f16(tmem + C::tDQ, sdesc_sw128(sK + k * 2048, BN * 128, 1024), sdesc_sw128(sDS + k * 2048, 0, 1024),
                      id_dq, k > 0);
-          else            // A = dS (MN-major over queries, chunks at BN*128), B = K (MN-major over d)
+          else
             umma_f16(tmem + C::tDQ, sdesc_sw128(sDS + k * 2048, BN * 128, 1024), sdesc_sw128(sK + k * 2048, 0, 1024),
                      id_dq, k > 0);
         }
@@ -227,39 +226,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < 4) {
-    // ================= compute warpgroup: thread = key row of the tile
-    const int j = warp * 32 + lane;
+  } else if (warp < 8) {
+    // ================= two compute warpgroups: thread = key row, warpgroup = half of the query columns
+    const int j = (warp % 4) * 32 + lane;
+    const int col0 = (warp / 4) * H;              // this warpgroup's first query column
     const int kvp = kv0 + j;                      // key position
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
     const float sl2 = a.scale * 1.4426950408889634f;
     const uint32_t sP = smem_u32(smem + C::kOffP), sDS = smem_u32(smem + C::kOffDS);
-    for (int n = 0; n < n_steps; ++n) {
+    const uint32_t sAux = smem_u32(aux);
+    StepIter it(qt_first, qt_last);
+    for (int n = 0; n < n_steps; ++n, it.next()) {
       const int st = n & 1;
-      const Step sp = step_of<D>(n, g, grp, qt_first, nqt, q_len);
-      const int qp_base = q_pos + sp.q0;          // position of the step's first query
+      const int qp_base = q_pos + it.qt * BQ + col0;        // position of this warpgroup's first query
+      const bool diag = kv0 + BN - 1 > qp_base;             // warp-uniform: causal mask needed
       mbar_wait(&bars->qdo_full[st], (n >> 1) & 1);
-      const float* lse2 = aux + st * BQ;
-      const float* dd = aux + 2 * BQ + st * BQ;
+      const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (2 * BQ + st * BQ + col0) * 4;
       mbar_wait(&bars->s_full, n & 1);
       tc_fence_after();
-      float p[BQ];
+      float p[H];
 #pragma unroll
-      for (int c = 0; c < BQ; c += 32) {
+      for (int c = 0; c < H; c += 32) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_base + C::tS + c, r);
+        tmem_ld32(tmem + lane_base + C::tS + col0 + c, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int qi = c + i;
-          const float e = ex2(fmaf(__uint_as_float(r[i]), sl2, -lse2[qi]));
-          p[qi] = (kvp <= qp_base + qi) ? e : 0.f;    // causal; invalid queries have lse2 = +inf
+        for (int i = 0; i < 32; i += 4) {
+          const float4 l4 = ld_shared_f4(a_lse + (c + i) * 4);
+          p[c + i + 0] = ex2(fmaf(__uint_as_float(r[i + 0]), sl2, -l4.x));
+          p[c + i + 1] = ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -l4.y));
+          p[c + i + 2] = ex2(fmaf(__uint_as_float(r[i + 2]), sl2, -l4.z));
+          p[c + i + 3] = ex2(fmaf(__uint_as_float(r[i + 3]), sl2, -l4.w));
         }
+      }
+      if (diag) {
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+          if (kvp > qp_base + i) p[i] = 0.f;               // causal (invalid queries: lse2 = +inf -> 0)
       }
       if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T smem free
 #pragma unroll
-      for (int c = 0; c < BQ; c += 8) {
-        const uint32_t addr = sP + (c / 64) * (BN * 128) + sw128_off(j, c % 64);
+      for (int c = 0; c < H; c += 8) {
+        const int cc = col0 + c;
+        const uint32_t addr = sP + (cc / 64) * (BN * 128) + sw128_off(j, cc % 64);
         st_shared_v4(addr, pack_bf16(p[c], p[c + 1]), pack_bf16(p[c + 2], p[c + 3]), pack_bf16(p[c + 4], p[c + 5]),
                      pack_bf16(p[c + 6], p[c + 7]));
       }
@@ -269,17 +278,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->dp_full, n & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < BQ; c += 32) {
+      for (int c = 0; c < H; c += 32) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_base + C::tDP + c, r);
+        tmem_ld32(tmem + lane_base + C::tDP + col0 + c, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) p[c + i] = p[c + i] * (__uint_as_float(r[i]) - dd[c + i]);
+        for (int i = 0; i < 32; i += 4) {
+          const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
+          p[c + i + 0] *= __uint_as_float(r[i + 0]) - d4.x;
+          p[c + i + 1] *= __uint_as_float(r[i + 1]) - d4.y;
+          p[c + i + 2] *= __uint_as_float(r[i + 2]) - d4.z;
+          p[c + i + 3] *= __uint_as_float(r[i + 3]) - d4.w;
+        }
       }
       if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem free
 #pragma unroll
-      for (int c = 0; c < BQ; c += 8) {
-        const uint32_t addr = sDS + (c / 64) * (BN * 128) + sw128_off(j, c % 64);
+      for (int c = 0; c < H; c += 8) {
+        const int cc = col0 + c;
+        const uint32_t addr = sDS + (cc / 64) * (BN * 128) + sw128_off(j, cc % 64);
         st_shared_v4(addr, pack_bf16(p[c], p[c + 1]), pack_bf16(p[c + 2], p[c + 3]), pack_bf16(p[c + 4], p[c + 5]),
                      pack_bf16(p[c + 6], p[c + 7]));
       }
@@ -287,49 +303,54 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->ds_full);
     }
-    // ---- dK, dV epilogue
+    // ---- dK, dV epilogue: warpgroup 0 stores dK, warpgroup 1 stores dV
     mbar_wait(&bars->dsq_done, (n_steps - 1) & 1);
     tc_fence_after();
     const bool valid = kvp < k_len;
     const size_t row = (size_t)(kst + kvp) * a.hkv + g;
+    const int which = warp / 4;
+    const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
+    const float mul = which == 0 ? a.scale : 1.f;
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
-      const float mul = which == 0 ? a.scale : 1.f;
+    for (int c = 0; c < D; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_base + tcol + c, r);
+      tmem_wait_ld();
+      if (!valid) continue;
+      if (accumulate) {
+        float* dst = reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D + c;
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + tcol + c, r);
-        tmem_wait_ld();
-        if (!valid) continue;
-        if (accumulate) {
-          float* dst = reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D + c;
+        for (int i = 0; i < 32; i += 4)
+          red_add_v4(dst + i, __uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul,
+                     __uint_as_float(r[i + 2]) * mul, __uint_as_float(r[i + 3]) * mul);
+      } else {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(which == 0 ? dk_out : dv_out) + row * D + c;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            red_add_v4(dst + i, __uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul,
-                       __uint_as_float(r[i + 2]) * mul, __uint_as_float(r[i + 3]) * mul);
-        } else {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(which == 0 ? dk_out : dv_out) + row * D + c;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul);
-            v.y = pack_bf16(__uint_as_float(r[i + 2]) * mul, __uint_as_float(r[i + 3]) * mul);
-            v.z = pack_bf16(__uint_as_float(r[i + 4]) * mul, __uint_as_float(r[i + 5]) * mul);
-            v.w = pack_bf16(__uint_as_float(r[i + 6]) * mul, __uint_as_float(r[i + 7]) * mul);
-            *reinterpret_cast<uint4*>(dst + i) = v;
-          }
+        for (int i = 0; i < 32; i += 8) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul);
+          v.y = pack_bf16(__uint_as_float(r[i + 2]) * mul, __uint_as_float(r[i + 3]) * mul);
+          v.z = pack_bf16(__uint_as_float(r[i + 4]) * mul, __uint_as_float(r[i + 5]) * mul);
+          v.w = pack_bf16(__uint_as_float(r[i + 6]) * mul, __uint_as_float(r[i + 7]) * mul);
+          *reinterpret_cast<uint4*>(dst + i) = v;
         }
       }
     }
-  } else if (warp < 8) {
-    // ================= dQ reduction warpgroup
-    const int t = (warp - 4) * 32 + lane;        // TMEM lane
-    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
-    for (int n = 0; n < n_steps; ++n) {
-      const Step sp = step_of<D>(n, g, grp, qt_first, nqt, q_len);
+  } else {
+    // ================= dQ warpgroup (warps 8-11): TMEM -> fp32 SW128 smem tile -> TMA reduce-add
+    const int t = (warp - 8) * 32 + lane;         // TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp - 8) * 32) << 16;
+    const uint32_t sDQ = smem_u32(smem + C::kOffDQ);
+    constexpr int kBoxes = D / 32;                 // 32-column fp32 boxes
+    constexpr int kBoxBytes = BQ * 128;
+    StepIter it(qt_first, qt_last);
+    for (int n = 0; n < n_steps; ++n, it.next()) {
+      const int h = g * grp + it.hi, q0 = it.qt * BQ;
       mbar_wait(&bars->dq_full, n & 1);
       tc_fence_after();
+      // the previous step's reduce must have finished reading the smem tile
+      if (t == 0) bulk_wait_read<0>();
+      named_bar_sync(1, 128);
       if (D == 128) {
         // dQ^T: lane = feature t, columns = queries of the step
 #pragma unroll
@@ -339,34 +360,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (c + i < sp.n_valid)
-              atomicAdd(dq_acc + ((size_t)(cu0 + sp.q0 + c + i) * a.hq + sp.h) * D + t,
-                        __uint_as_float(r[i]) * a.scale);
+            st_shared_f32(sDQ + (t / 32) * kBoxBytes + sw128_off_f32(c + i, t % 32), __uint_as_float(r[i]) * a.scale);
         }
       } else {
         // dQ: lane = query row t, columns = features
-        const bool ok = t < sp.n_valid;
-        float* dst = dq_acc + ((size_t)(cu0 + sp.q0 + t) * a.hq + sp.h) * D;
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
           uint32_t r[32];
           tmem_ld32(tmem + lane_base + C::tDQ + c, r);
           tmem_wait_ld();
-          if (ok) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              red_add_v4(dst + c + i, __uint_as_float(r[i]) * a.scale, __uint_as_float(r[i + 1]) * a.scale,
-                         __uint_as_float(r[i + 2]) * a.scale, __uint_as_float(r[i + 3]) * a.scale);
-          }
+          for (int i = 0; i < 32; i += 4)
+            st_shared_f4(sDQ + (c / 32) * kBoxBytes + sw128_off_f32(t, i), __uint_as_float(r[i]) * a.scale,
+                         __uint_as_float(r[i + 1]) * a.scale, __uint_as_float(r[i + 2]) * a.scale,
+                         __uint_as_float(r[i + 3]) * a.scale);
         }
       }
       tc_fence_before();
-      mbar_arrive(&bars->dq_empty);
+      mbar_arrive(&bars->dq_empty);                // TMEM dQ columns may be overwritten
+      fence_async_smem();
+      named_bar_sync(1, 128);
+      if (t == 0) {
+#pragma unroll
+        for (int b = 0; b < kBoxes; ++b) tma_reduce_add_2d(&tm_dq, smem + C::kOffDQ + b * kBoxBytes, h * D + b * 32, cu0 + q0);
+        bulk_commit();
+      }
     }
+    if (t == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == 13) tmem_dealloc<512>(tmem);
 }
 
 // D[h][r] = sum_c dO[r][h][c] * O[r][h][c] (bf16 in, fp32 out); zero the dQ accumulator rows.
@@ -437,24 +461,25 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
     if (skr_status e = launch_status("attn bwd preprocess")) return e;
   }
   if (a.n_tiles > 0) {
-    CUtensorMap tq, tk, tv, tdo;
+    CUtensorMap tq, tk, tv, tdo, tdq;
     const uint64_t qcols = (uint64_t)a.hq * d, kcols = (uint64_t)a.hkv * d;
     const uint32_t bq = d == 128 ? 64 : 128;
     if (!make_tmap_2d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, bq, 64, true) ||
         !make_tmap_2d(&tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, bq, 64, true) ||
         !make_tmap_2d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true) ||
-        !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true))
+        !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true) ||
+        !make_tmap_2d(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n_q_rows, qcols, qcols, bq, 32, true))
       return fail(SKR_E_CUDA, "attn bwd: tensor map encode failed");
     dim3 grid(a.hkv, a.n_tiles);
     if (d == 128) {
       constexpr int smem = bwd::Cfg<128>::kSmem;
       cudaFuncSetAttribute(bwd::attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      bwd::attn_bwd_kernel<128><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, a, lse, Dbuf, dq_acc, dk, dv,
+      bwd::attn_bwd_kernel<128><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv,
                                                                    accumulate);
     } else {
       constexpr int smem = bwd::Cfg<64>::kSmem;
       cudaFuncSetAttribute(bwd::attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      bwd::attn_bwd_kernel<64><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, a, lse, Dbuf, dq_acc, dk, dv,
+      bwd::attn_bwd_kernel<64><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv,
                                                                   accumulate);
     }
     if (skr_status e = launch_status("attn_bwd_kernel")) return e;
