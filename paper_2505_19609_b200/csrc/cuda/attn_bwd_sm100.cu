@@ -15,8 +15,8 @@
 // query columns [w*BQ/2, (w+1)*BQ/2): P^T, dS^T from TMEM -> bf16 swizzled smem), warps 8-11 dQ
 // (TMEM -> scaled fp32 SW128 smem tile -> one TMA bulk reduce-add per 32-column box into the fp32
 // dQ accumulator), warp 12 TMA producer (K, V once; Q/dO ring of 2 + LSE/D rows), warp 13 MMA.
-// MMA order per step n:  S(n) dP(n) | P(n) -> dV(n) S(n+1) | dS(n) -> dK(n) dQ(n) dP(n+1)
-// so the tensor core works on one half of the step while the compute warpgroup does the other.
+// MMA order per step n: S(n+1) as soon as S(n) is read | dV(n) after P(n) | dP(n+1) as soon as dP(n)
+// is read | dK(n) dQ(n) after dS(n): the tensor core runs ahead while the compute warpgroups work.
 #include "attn_common.cuh"
 #include "device.cuh"
 #include "sm100.cuh"
@@ -60,6 +60,7 @@ struct Bars {
   uint64_t kv_full;
   uint64_t qdo_full[2], qdo_empty[2];
   uint64_t s_full, dp_full, p_full, ds_full, dv_done, dsq_done, dq_full, dq_empty;
+  uint64_t s_free, dp_free;
   uint32_t tmem_base;
 };
 
@@ -108,6 +109,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->dsq_done, 1);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_empty, 128);
+    mbar_init(&bars->s_free, kComputeThreads);
+    mbar_init(&bars->dp_free, kComputeThreads);
     fence_mbar_init();
   }
   if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
@@ -130,10 +133,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(smem + C::kOffV + c * BN * 128, &tm_v, &bars->kv_full, g * D + c * 64, kst + kv0);
       }
     }
+    // LSE / D of a step are fetched into registers one step ahead, so their global-load latency
+    // overlaps the wait for the stage to free up instead of delaying the compute warpgroups.
+    constexpr int kPer = BQ / 32;
+    float pl[kPer], pd[kPer];
+    auto fetch = [&](const StepIter& s_) {
+      const int h = g * grp + s_.hi, q0 = s_.qt * BQ, nv = min(BQ, q_len - q0);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = lane + 32 * u;
+        const size_t off = (size_t)h * a.ld_lse + cu0 + q0 + i;
+        pl[u] = i < nv ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
+        pd[u] = i < nv ? Dbuf[off] : 0.f;
+      }
+    };
     StepIter it(qt_first, qt_last);
-    for (int n = 0; n < n_steps; ++n, it.next()) {
+    fetch(it);
+    for (int n = 0; n < n_steps; ++n) {
       const int st = n & 1;
-      const int h = g * grp + it.hi, q0 = it.qt * BQ, nv = min(BQ, q_len - q0);
+      const int h = g * grp + it.hi, q0 = it.qt * BQ;
       mbar_wait(&bars->qdo_empty[st], ((n >> 1) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&bars->qdo_full[st], 2 * C::kQBytes);
@@ -144,14 +162,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                       h * D + c * 64, cu0 + q0);
         }
       }
-      for (int i = lane; i < BQ; i += 32) {
-        const bool ok = i < nv;
-        const size_t off = (size_t)h * a.ld_lse + cu0 + q0 + i;
-        aux[st * BQ + i] = ok ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
-        aux[2 * BQ + st * BQ + i] = ok ? Dbuf[off] : 0.f;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        aux[st * BQ + lane + 32 * u] = pl[u];
+        aux[2 * BQ + st * BQ + lane + 32 * u] = pd[u];
       }
       __syncwarp();
       mbar_arrive(&bars->qdo_full[st]);
+      it.next();
+      if (n + 1 < n_steps) fetch(it);
     }
   } else if (warp == 13) {
     // ================= MMA issuer
@@ -198,18 +217,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&bars->s_full);
       issue_t(sV, sDO, C::tDP);
       umma_commit(&bars->dp_full);
+      // S(n+1) / dP(n+1) are issued as soon as the compute warpgroups have read S(n) / dP(n) out of
+      // TMEM, so they run on the tensor core while the elementwise work of step n is still going.
       for (int n = 0; n < n_steps; ++n) {
         const int st = n & 1, st1 = (n + 1) & 1;
         const bool more = n + 1 < n_steps;
-        mbar_wait(&bars->p_full, n & 1);
-        tc_fence_after();
-        issue_kv(sP, sDO + st * C::kQBytes, C::tDV, n > 0);
-        umma_commit(&bars->dv_done);
+        mbar_wait(&bars->s_free, n & 1);
         if (more) {
           mbar_wait(&bars->qdo_full[st1], ((n + 1) >> 1) & 1);
           tc_fence_after();
           issue_t(sK, sQ + st1 * C::kQBytes, C::tS);
           umma_commit(&bars->s_full);
+        }
+        mbar_wait(&bars->p_full, n & 1);
+        tc_fence_after();
+        issue_kv(sP, sDO + st * C::kQBytes, C::tDV, n > 0);
+        umma_commit(&bars->dv_done);
+        mbar_wait(&bars->dp_free, n & 1);
+        if (more) {
+          tc_fence_after();
+          issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
+          umma_commit(&bars->dp_full);
         }
         mbar_wait(&bars->ds_full, n & 1);
         tc_fence_after();
@@ -220,10 +248,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bars->dq_full);
         umma_commit(&bars->dsq_done);
         umma_commit(&bars->qdo_empty[st]);
-        if (more) {
-          issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
-          umma_commit(&bars->dp_full);
-        }
       }
     }
   } else if (warp < 8) {
@@ -251,13 +275,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tmem + lane_base + C::tS + col0 + c, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 l4 = ld_shared_f4(a_lse + (c + i) * 4);
-          p[c + i + 0] = ex2(fmaf(__uint_as_float(r[i + 0]), sl2, -l4.x));
-          p[c + i + 1] = ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -l4.y));
-          p[c + i + 2] = ex2(fmaf(__uint_as_float(r[i + 2]), sl2, -l4.z));
-          p[c + i + 3] = ex2(fmaf(__uint_as_float(r[i + 3]), sl2, -l4.w));
-        }
+        for (int i = 0; i < 32; ++i) p[c + i] = __uint_as_float(r[i]);
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->s_free);                   // S TMEM may be overwritten by S(n+1)
+#pragma unroll
+      for (int i = 0; i < H; i += 4) {
+        const float4 l4 = ld_shared_f4(a_lse + i * 4);
+        p[i + 0] = ex2(fmaf(p[i + 0], sl2, -l4.x));
+        p[i + 1] = ex2(fmaf(p[i + 1], sl2, -l4.y));
+        p[i + 2] = ex2(fmaf(p[i + 2], sl2, -l4.z));
+        p[i + 3] = ex2(fmaf(p[i + 3], sl2, -l4.w));
       }
       if (diag) {
 #pragma unroll
@@ -282,6 +310,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmem_ld32(tmem + lane_base + C::tDP + col0 + c, r);
         tmem_wait_ld();
+        if (c + 32 >= H) {
+          tc_fence_before();
+          mbar_arrive(&bars->dp_free);              // dP TMEM may be overwritten by dP(n+1)
+        }
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);

@@ -6,7 +6,8 @@
 //   warps 0-3  softmax warpgroup A (head ha), thread t owns query row t of the tile
 //   warps 4-7  softmax warpgroup B (head hb = ha + 1, if it exists in the group)
 //   warp 8     TMA producer: Q tiles once, then a ring of K/V tiles (SW128, 64-col boxes)
-//   warp 9     MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM
+//   warp 9     MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM; S(j+1) is issued as
+//              soon as the softmax has read S(j) (s_free), overlapping the exponentials of tile j
 // TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+d) O_B [384,384+d).
 // Softmax: S row read with tcgen05.ld (no shuffles: one thread = one row), exp2 with the scale
 // folded in, running max kept in log2 units and O rescaled in TMEM only when the max grows by
@@ -24,6 +25,7 @@ namespace fwd {
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kPolyPer8 = 3;               // exponentials per 8 computed by ex2_poly
 
 template <int D>
 struct Cfg {
@@ -42,7 +44,7 @@ struct Cfg {
 struct Bars {
   uint64_t q_full;
   uint64_t kv_full[4], kv_empty[4];
-  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint64_t s_full[2], s_free[2], p_full[2], pv_done[2];
   uint32_t tmem_base;
 };
 
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars->s_full[s], 1);
+      mbar_init(&bars->s_free[s], 128);
       mbar_init(&bars->p_full[s], 128);
       mbar_init(&bars->pv_done[s], 1);
     }
@@ -144,40 +147,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       mbar_wait(&bars->q_full, 0);
       tc_fence_after();
-      // tile 0: S for both heads
-      int it = 0;
-      {
-        const int u = it % C::kUnits;
-        mbar_wait(&bars->kv_full[u], (it / C::kUnits) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = sKV + u * C::kKVBytes;
-        for (int s = 0; s < nq; ++s) issue_s(s, k_addr);
-        umma_commit(&bars->kv_empty[u]);
-        ++it;
-      }
-      for (int j = 1; j <= n_kv; ++j) {
-        // V of tile j-1
-        const int uv = it % C::kUnits;
-        mbar_wait(&bars->kv_full[uv], (it / C::kUnits) & 1);
-        ++it;
-        const uint32_t v_addr = sKV + uv * C::kKVBytes;
-        int uk = -1;
-        uint32_t k_addr = 0;
-        if (j < n_kv) {
-          uk = it % C::kUnits;
-          mbar_wait(&bars->kv_full[uk], (it / C::kUnits) & 1);
-          ++it;
-          k_addr = sKV + uk * C::kKVBytes;
+      // KV units arrive in the order K0 V0 K1 V1 ...; S(j+1) is issued as soon as the softmax has read
+      // S(j) out of TMEM (s_free), so it overlaps the exponentials of tile j; PV(j) after P(j).
+      mbar_wait(&bars->kv_full[0], 0);
+      tc_fence_after();
+      for (int s = 0; s < nq; ++s) issue_s(s, sKV);
+      umma_commit(&bars->kv_empty[0]);
+      for (int j = 0; j < n_kv; ++j) {
+        const int itv = 2 * j + 1, itk = 2 * j + 2;      // ring positions of V(j) and K(j+1)
+        if (j + 1 < n_kv) {
+          const int uk = itk % C::kUnits;
+          mbar_wait(&bars->kv_full[uk], (itk / C::kUnits) & 1);
+          for (int s = 0; s < nq; ++s) {
+            mbar_wait(&bars->s_free[s], j & 1);
+            tc_fence_after();
+            issue_s(s, sKV + uk * C::kKVBytes);
+          }
+          umma_commit(&bars->kv_empty[uk]);
         }
-        tc_fence_after();
+        const int uv = itv % C::kUnits;
+        mbar_wait(&bars->kv_full[uv], (itv / C::kUnits) & 1);
         for (int s = 0; s < nq; ++s) {
-          mbar_wait(&bars->p_full[s], (j - 1) & 1);     // P_s(j-1) in smem, S_s(j-1) consumed, O_s corrected
+          mbar_wait(&bars->p_full[s], j & 1);            // P_s(j) in smem, O_s corrected
           tc_fence_after();
-          issue_pv(s, v_addr, j > 1);
-          if (j < n_kv) issue_s(s, k_addr);
+          issue_pv(s, sKV + uv * C::kKVBytes, j > 0);
         }
         umma_commit(&bars->kv_empty[uv]);
-        if (uk >= 0) umma_commit(&bars->kv_empty[uk]);
       }
     }
   } else {
@@ -206,15 +201,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[c + i] = __uint_as_float(r[i]);
         }
+        tc_fence_before();
+        mbar_arrive(&bars->s_free[s]);        // S_s TMEM may now take S_s(j+1)
         const int kv0 = j * BN;
         if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
 #pragma unroll
           for (int i = 0; i < BN; ++i)
             if (kv0 + i > qp) x[i] = -INFINITY;
         }
-        float mx = -INFINITY;
+        // row max with 8 independent chains (a single 128-long fmax chain is ~512 cycles of latency)
+        float mxs[8];
 #pragma unroll
-        for (int i = 0; i < BN; ++i) mx = fmaxf(mx, x[i]);
+        for (int i = 0; i < 8; ++i) mxs[i] = x[i];
+#pragma unroll
+        for (int i = 8; i < BN; ++i) mxs[i % 8] = fmaxf(mxs[i % 8], x[i]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                               fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
         const float m_new = fmaxf(m_ref, mx * sl2);
         // P_s(j-1) consumed and O_s(j-1) accumulated before P / O are touched again
         if (j > 0) {
@@ -242,18 +244,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // P = exp2(S * scale * log2e - m_ref), row sum, bf16 into swizzled smem (K-major A operand)
         const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};               // 4 independent row-sum chains
 #pragma unroll
         for (int c = 0; c < BN; c += 8) {
           float pv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            pv[i] = ex2(fmaf(x[c + i], sl2, neg_m));
-            l += pv[i];
+            const float xx = fmaf(x[c + i], sl2, neg_m);
+            // 3 of every 8 exponentials on the FMA pipe, 5 on MUFU (MUFU ex2 is the d=64 bound)
+            pv[i] = (i % 8) < kPolyPer8 ? ex2_poly(xx) : ex2(xx);
+            ls[i % 4] += pv[i];
           }
           const uint32_t addr = sP_u32 + (c / 64) * (BM * 128) + sw128_off(row, c % 64);
           st_shared_v4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
                        pack_bf16(pv[6], pv[7]));
         }
+        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
