@@ -204,7 +204,7 @@ skr_status skr_comm_all_reduce_f32(skr_comm* c, float* buf, size_t count, void* 
 /* ------------------------------------------------------------------ diagnostics */
 /* UMMA/TMA/TMEM building-block self-test: C[128][n] fp32 from bf16 A/B with operand layout
  * `variant` (0: A K-major, B K-major; 1: B MN-major; 2: A and B MN-major; 3: A written by threads
- * into swizzled smem). n in {64,128}, K = 128. */
+ * into swizzled smem; 4: A written by threads into TMEM, MMA A operand from TMEM). n in {64,128}, K = 128. */
 skr_status skr_selftest_umma(int32_t variant, int32_t n, const void* A, const void* B, float* C, void* stream);
 
 #ifdef __cplusplus

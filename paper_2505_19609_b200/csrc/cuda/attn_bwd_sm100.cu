@@ -33,6 +33,7 @@ template <int D>
 struct Cfg {
   static constexpr int BQ = D == 128 ? 64 : 128;         // query step
   static constexpr int H = BQ / 2;                       // columns per compute warpgroup
+  static constexpr int kStages = 3;                      // Q/dO (+LSE/D) ring depth
   static constexpr int kChunks = D / 64;
   static constexpr int kKVBytes = BN * D * 2;
   static constexpr int kQBytes = BQ * D * 2;
@@ -40,25 +41,32 @@ struct Cfg {
   static constexpr int kDQBytes = BQ * D * 4;            // fp32 dQ tile, SW128 boxes of 32 columns
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kKVBytes;
-  static constexpr int kOffQ = kOffV + kKVBytes;          // [2] stages
-  static constexpr int kOffDO = kOffQ + 2 * kQBytes;      // [2] stages
-  static constexpr int kOffP = kOffDO + 2 * kQBytes;
-  static constexpr int kOffDS = kOffP + kPBytes;
+  static constexpr int kOffQ = kOffV + kKVBytes;          // [kStages]
+  static constexpr int kOffDO = kOffQ + kStages * kQBytes; // [kStages]
+  static constexpr int kOffDS = kOffDO + kStages * kQBytes;
   static constexpr int kOffDQ = kOffDS + kPBytes;
-  static constexpr int kOffAux = kOffDQ + kDQBytes;       // lse2[2][BQ], dd[2][BQ] fp32
-  static constexpr int kOffBar = kOffAux + 4 * BQ * 4;
+  static constexpr int kOffAux = kOffDQ + kDQBytes;       // lse2[kStages][BQ], dd[kStages][BQ] fp32
+  static constexpr int kOffBar = kOffAux + 2 * kStages * BQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
-  // TMEM columns
+  // TMEM columns. P^T and dS^T (bf16 pairs) are the A operands of dV / dK straight from TMEM.
+  //  d = 128: S^T[0,64) dP^T[64,128) dQ^T[128,192) P^T[192,224) dS^T[224,256) dV[256,384) dK[384,512)
+  //  d =  64: S^T[0,128) dP^T[128,256) dQ[256,320) dV[320,384) dK[384,448) P^T[448,512);
+  //           dS^T aliases dP^T: warpgroup w packs its 64 columns into [128+64w, 160+64w)
+  static constexpr bool kDSAlias = D == 64;
   static constexpr int tS = 0;
   static constexpr int tDP = BQ;
   static constexpr int tDQ = 2 * BQ;
   static constexpr int tDV = D == 128 ? 256 : 320;
   static constexpr int tDK = 384;
+  static constexpr int tPT = D == 128 ? 192 : 448;
+  // packed column of query pair-column q/2 for P^T / dS^T, per warpgroup half
+  __device__ static constexpr int tDS(int w) { return kDSAlias ? 128 + 64 * w : 224 + (H / 2) * w; }
+  __device__ static constexpr int tPTw(int w) { return tPT + (H / 2) * w; }
 };
 
 struct Bars {
   uint64_t kv_full;
-  uint64_t qdo_full[2], qdo_empty[2];
+  uint64_t qdo_full[3], qdo_empty[3];
   uint64_t s_full, dp_full, p_full, ds_full, dv_done, dsq_done, dq_full, dq_empty;
   uint64_t s_free, dp_free;
   uint32_t tmem_base;
@@ -85,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
-  float* aux = reinterpret_cast<float*>(smem + C::kOffAux);  // lse2[2][BQ] then dd[2][BQ]
+  float* aux = reinterpret_cast<float*>(smem + C::kOffAux);  // lse2[kStages][BQ] then dd[kStages][BQ]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   const int g = blockIdx.x;
@@ -100,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&bars->qdo_full[s], 33), mbar_init(&bars->qdo_empty[s], 1);
+    for (int s = 0; s < C::kStages; ++s) mbar_init(&bars->qdo_full[s], 33), mbar_init(&bars->qdo_empty[s], 1);
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->p_full, kComputeThreads);
@@ -150,9 +158,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     StepIter it(qt_first, qt_last);
     fetch(it);
     for (int n = 0; n < n_steps; ++n) {
-      const int st = n & 1;
+      const int st = n % C::kStages;
       const int h = g * grp + it.hi, q0 = it.qt * BQ;
-      mbar_wait(&bars->qdo_empty[st], ((n >> 1) & 1) ^ 1);
+      mbar_wait(&bars->qdo_empty[st], ((n / C::kStages) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&bars->qdo_full[st], 2 * C::kQBytes);
         for (int c = 0; c < C::kChunks; ++c) {
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         aux[st * BQ + lane + 32 * u] = pl[u];
-        aux[2 * BQ + st * BQ + lane + 32 * u] = pd[u];
+        aux[C::kStages * BQ + st * BQ + lane + 32 * u] = pd[u];
       }
       __syncwarp();
       mbar_arrive(&bars->qdo_full[st]);
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t sK = smem_u32(smem + C::kOffK), sV = smem_u32(smem + C::kOffV);
       const uint32_t sQ = smem_u32(smem + C::kOffQ), sDO = smem_u32(smem + C::kOffDO);
-      const uint32_t sP = smem_u32(smem + C::kOffP), sDS = smem_u32(smem + C::kOffDS);
+      const uint32_t sDS = smem_u32(smem + C::kOffDS);
       const uint32_t id_sdp = idesc_bf16_f32(BN, BQ, 0, 0);   // S^T = K Q^T, dP^T = V dO^T
       const uint32_t id_kv = idesc_bf16_f32(BN, D, 0, 1);     // dV += P^T dO, dK += dS^T Q
       // dQ^T = K^T dS^T (d = 128) or dQ = dS K (d = 64): both operands MN-major
@@ -191,12 +199,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                    k > 0);
         }
       };
-      auto issue_kv = [&](uint32_t a_base, uint32_t b_base, uint32_t tcol, bool acc) {
+      // dV / dK: A = P^T or dS^T from TMEM (k-step = 16 queries = 8 packed columns of one warpgroup
+      // half), B = dO or Q tile (MN-major over d)
+      auto issue_kv = [&](bool is_dk, uint32_t b_base, uint32_t tcol, bool acc) {
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k) {
-          const uint32_t ao = (k / 4) * (BN * 128) + (k % 4) * 32;
-          umma_f16(tmem + tcol, sdesc_sw128(a_base + ao, 16, 1024), sdesc_sw128(b_base + k * 2048, BQ * 128, 1024),
-                   id_kv, acc || k > 0);
+          const int w = (k * 16) / H, kk = (k * 16) % H;
+          const uint32_t a_col = (is_dk ? C::tDS(w) : C::tPTw(w)) + kk / 2;
+          umma_f16_ts(tmem + tcol, tmem + a_col, sdesc_sw128(b_base + k * 2048, BQ * 128, 1024), id_kv, acc || k > 0);
         }
       };
       auto issue_dq = [&]() {
@@ -217,37 +227,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&bars->s_full);
       issue_t(sV, sDO, C::tDP);
       umma_commit(&bars->dp_full);
-      // S(n+1) / dP(n+1) are issued as soon as the compute warpgroups have read S(n) / dP(n) out of
-      // TMEM, so they run on the tensor core while the elementwise work of step n is still going.
+      // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its own
+      // columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows dK(n)
+      // in the in-order tensor pipe.
       for (int n = 0; n < n_steps; ++n) {
-        const int st = n & 1, st1 = (n + 1) & 1;
+        const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
         const bool more = n + 1 < n_steps;
         mbar_wait(&bars->s_free, n & 1);
         if (more) {
-          mbar_wait(&bars->qdo_full[st1], ((n + 1) >> 1) & 1);
+          mbar_wait(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
           tc_fence_after();
           issue_t(sK, sQ + st1 * C::kQBytes, C::tS);
           umma_commit(&bars->s_full);
         }
         mbar_wait(&bars->p_full, n & 1);
         tc_fence_after();
-        issue_kv(sP, sDO + st * C::kQBytes, C::tDV, n > 0);
+        issue_kv(false, sDO + st * C::kQBytes, C::tDV, n > 0);
         umma_commit(&bars->dv_done);
-        mbar_wait(&bars->dp_free, n & 1);
-        if (more) {
-          tc_fence_after();
-          issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
-          umma_commit(&bars->dp_full);
+        if (!C::kDSAlias) {
+          mbar_wait(&bars->dp_free, n & 1);
+          if (more) {
+            tc_fence_after();
+            issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
+            umma_commit(&bars->dp_full);
+          }
         }
         mbar_wait(&bars->ds_full, n & 1);
         tc_fence_after();
-        issue_kv(sDS, sQ + st * C::kQBytes, C::tDK, n > 0);
+        issue_kv(true, sQ + st * C::kQBytes, C::tDK, n > 0);
         mbar_wait(&bars->dq_empty, (n & 1) ^ 1);
         tc_fence_after();
         issue_dq();
         umma_commit(&bars->dq_full);
         umma_commit(&bars->dsq_done);
         umma_commit(&bars->qdo_empty[st]);
+        if (C::kDSAlias && more) {
+          issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
+          umma_commit(&bars->dp_full);
+        }
       }
     }
   } else if (warp < 8) {
@@ -257,15 +274,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kvp = kv0 + j;                      // key position
     const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
     const float sl2 = a.scale * 1.4426950408889634f;
-    const uint32_t sP = smem_u32(smem + C::kOffP), sDS = smem_u32(smem + C::kOffDS);
+    const uint32_t sDS = smem_u32(smem + C::kOffDS);
     const uint32_t sAux = smem_u32(aux);
+    const int wg = warp / 4;
     StepIter it(qt_first, qt_last);
     for (int n = 0; n < n_steps; ++n, it.next()) {
-      const int st = n & 1;
+      const int st = n % C::kStages;
       const int qp_base = q_pos + it.qt * BQ + col0;        // position of this warpgroup's first query
       const bool diag = kv0 + BN - 1 > qp_base;             // warp-uniform: causal mask needed
-      mbar_wait(&bars->qdo_full[st], (n >> 1) & 1);
-      const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (2 * BQ + st * BQ + col0) * 4;
+      mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1);
+      const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (C::kStages * BQ + st * BQ + col0) * 4;
       mbar_wait(&bars->s_full, n & 1);
       tc_fence_after();
       float p[H];
@@ -292,15 +310,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < H; ++i)
           if (kvp > qp_base + i) p[i] = 0.f;               // causal (invalid queries: lse2 = +inf -> 0)
       }
-      if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T smem free
+      if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T TMEM columns free
+      tc_fence_after();
+      {
+        uint32_t pk[H / 2];
 #pragma unroll
-      for (int c = 0; c < H; c += 8) {
-        const int cc = col0 + c;
-        const uint32_t addr = sP + (cc / 64) * (BN * 128) + sw128_off(j, cc % 64);
-        st_shared_v4(addr, pack_bf16(p[c], p[c + 1]), pack_bf16(p[c + 2], p[c + 3]), pack_bf16(p[c + 4], p[c + 5]),
-                     pack_bf16(p[c + 6], p[c + 7]));
+        for (int i = 0; i < H / 2; ++i) pk[i] = pack_bf16(p[2 * i], p[2 * i + 1]);
+        tmem_st_half<H / 2>(tmem + lane_base + C::tPTw(wg), pk);
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
       mbar_wait(&bars->dp_full, n & 1);
@@ -323,14 +341,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           p[c + i + 3] *= __uint_as_float(r[i + 3]) - d4.w;
         }
       }
-      if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem free
+      if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem / TMEM free
+      tc_fence_after();
+      {
+        uint32_t pk[H / 2];
 #pragma unroll
-      for (int c = 0; c < H; c += 8) {
-        const int cc = col0 + c;
-        const uint32_t addr = sDS + (cc / 64) * (BN * 128) + sw128_off(j, cc % 64);
-        st_shared_v4(addr, pack_bf16(p[c], p[c + 1]), pack_bf16(p[c + 2], p[c + 3]), pack_bf16(p[c + 4], p[c + 5]),
-                     pack_bf16(p[c + 6], p[c + 7]));
+        for (int i = 0; i < H / 2; ++i) pk[i] = pack_bf16(p[2 * i], p[2 * i + 1]);
+        tmem_st_half<H / 2>(tmem + lane_base + C::tDS(wg), pk);   // A operand of dK
+#pragma unroll
+        for (int c = 0; c < H; c += 8) {                             // B (d = 128) / A (d = 64) of dQ
+          const int cc = col0 + c;
+          const uint32_t addr = sDS + (cc / 64) * (BN * 128) + sw128_off(j, cc % 64);
+          st_shared_v4(addr, pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]);
+        }
       }
+      tmem_wait_st();
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->ds_full);

@@ -8,11 +8,12 @@
 //   warp 8     TMA producer: Q tiles once, then a ring of K/V tiles (SW128, 64-col boxes)
 //   warp 9     MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM; S(j+1) is issued as
 //              soon as the softmax has read S(j) (s_free), overlapping the exponentials of tile j
-// TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+d) O_B [384,384+d).
+// TMEM (512 cols): see Cfg.
 // Softmax: S row read with tcgen05.ld (no shuffles: one thread = one row), exp2 with the scale
 // folded in, running max kept in log2 units and O rescaled in TMEM only when the max grows by
-// more than 8 (exact: the final normalisation uses the same reference max), P written as bf16 into
-// swizzled smem (K-major A operand of the PV MMA). Causal: only KV tiles up to the tile's last
+// more than 8 (exact: the final normalisation uses the same reference max), P written as bf16 pairs
+// into TMEM with tcgen05.st and fed to the PV MMA as its A operand straight from TMEM (no smem
+// traffic: with single-CTA M=128 MMAs the SS operand reads alone saturate shared memory). Causal: only KV tiles up to the tile's last
 // query are visited (bottom-right aligned with q_pos, R23); the diagonal tiles are masked.
 #include "attn_common.cuh"
 #include "device.cuh"
@@ -32,18 +33,23 @@ struct Cfg {
   static constexpr int kChunks = D / 64;                 // 64-col SW128 boxes per row
   static constexpr int kQBytes = BM * D * 2;             // one Q tile
   static constexpr int kKVBytes = BN * D * 2;            // one K or V tile
-  static constexpr int kUnits = D == 128 ? 3 : 4;        // K/V ring depth (units of one tile)
-  static constexpr int kPBytes = BM * BN * 2;            // P tile (bf16)
+  static constexpr int kUnits = D == 128 ? 4 : 6;        // K/V ring depth (units of one tile), <= 8
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQBytes;
-  static constexpr int kOffP = kOffKV + kUnits * kKVBytes;
-  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  static constexpr int kOffBar = kOffKV + kUnits * kKVBytes;
   static constexpr int kSmem = kOffBar + 256 + 1024;    // + barriers + alignment slack
+  // TMEM columns. P (bf16 pairs) is the A operand of O += P V straight from TMEM (no smem traffic).
+  // d = 64 : S_A[0,128) S_B[128,256) O_A[256,320) O_B[320,384) P_A[384,448) P_B[448,512)
+  // d = 128: S_A[0,128) S_B[128,256) O_A[256,384) O_B[384,512); P_s aliases the first 64 cols of S_s
+  static constexpr bool kPAlias = D == 128;
+  __device__ static constexpr uint32_t tS(int s) { return s * 128; }
+  __device__ static constexpr uint32_t tO(int s) { return 256 + s * D; }
+  __device__ static constexpr uint32_t tP(int s) { return kPAlias ? s * 128 : 384 + s * 64; }
 };
 
-struct Bars {
+struct Bars {  // kUnits <= 8
   uint64_t q_full;
-  uint64_t kv_full[4], kv_empty[4];
+  uint64_t kv_full[8], kv_empty[8];
   uint64_t s_full[2], s_free[2], p_full[2], pv_done[2];
   uint32_t tmem_base;
 };
@@ -123,26 +129,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0);   // S = Q K^T   (both K-major)
       const uint32_t id_o = idesc_bf16_f32(BM, D, 0, 1);    // O += P V    (V is MN-major)
       const uint32_t sQ = smem_u32(smem + C::kOffQ), sKV = smem_u32(smem + C::kOffKV);
-      const uint32_t sP = smem_u32(smem + C::kOffP);
       auto issue_s = [&](int s, uint32_t k_addr) {
         const uint32_t q_addr = sQ + s * C::kQBytes;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k / 4) * (BM * 128) + (k % 4) * 32;
           const uint32_t koff = (k / 4) * (BN * 128) + (k % 4) * 32;
-          umma_f16(tmem + s * 128, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + koff, 16, 1024), id_s,
+          umma_f16(tmem + C::tS(s), sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + koff, 16, 1024), id_s,
                    k > 0);
         }
         umma_commit(&bars->s_full[s]);
       };
       auto issue_pv = [&](int s, uint32_t v_addr, bool acc) {
-        const uint32_t p_addr = sP + s * C::kPBytes;
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) {
-          const uint32_t poff = (k / 4) * (BM * 128) + (k % 4) * 32;
-          umma_f16(tmem + 256 + s * 128, sdesc_sw128(p_addr + poff, 16, 1024),
-                   sdesc_sw128(v_addr + k * 2048, BN * 128, 1024), id_o, acc || k > 0);
-        }
+        for (int k = 0; k < BN / 16; ++k)
+          umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, sdesc_sw128(v_addr + k * 2048, BN * 128, 1024), id_o,
+                      acc || k > 0);
         umma_commit(&bars->pv_done[s]);
       };
       mbar_wait(&bars->q_full, 0);
@@ -155,8 +157,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&bars->kv_empty[0]);
       for (int j = 0; j < n_kv; ++j) {
         const int itv = 2 * j + 1, itk = 2 * j + 2;      // ring positions of V(j) and K(j+1)
-        if (j + 1 < n_kv) {
-          const int uk = itk % C::kUnits;
+        const bool more = j + 1 < n_kv;
+        const int uk = itk % C::kUnits, uv = itv % C::kUnits;
+        if (!C::kPAlias && more) {
+          // separate P columns: S(j+1) as soon as the softmax has read S(j)
           mbar_wait(&bars->kv_full[uk], (itk / C::kUnits) & 1);
           for (int s = 0; s < nq; ++s) {
             mbar_wait(&bars->s_free[s], j & 1);
@@ -165,14 +169,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma_commit(&bars->kv_empty[uk]);
         }
-        const int uv = itv % C::kUnits;
         mbar_wait(&bars->kv_full[uv], (itv / C::kUnits) & 1);
+        if (C::kPAlias && more) mbar_wait(&bars->kv_full[uk], (itk / C::kUnits) & 1);
         for (int s = 0; s < nq; ++s) {
-          mbar_wait(&bars->p_full[s], j & 1);            // P_s(j) in smem, O_s corrected
+          mbar_wait(&bars->p_full[s], j & 1);            // P_s(j) in TMEM, O_s corrected
           tc_fence_after();
           issue_pv(s, sKV + uv * C::kKVBytes, j > 0);
+          // P aliases S: S(j+1) enters the (in-order) tensor pipe after PV(j) has read P(j)
+          if (C::kPAlias && more) issue_s(s, sKV + uk * C::kKVBytes);
         }
         umma_commit(&bars->kv_empty[uv]);
+        if (C::kPAlias && more) umma_commit(&bars->kv_empty[uk]);
       }
     }
   } else {
@@ -182,13 +189,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (h >= 0) {
       const int row = (warp % 4) * 32 + lane;  // TMEM lane == query row of the tile
       const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
-      const uint32_t tS = tmem + lane_base + s * 128;
-      const uint32_t tO = tmem + lane_base + 256 + s * 128;
+      const uint32_t tS = tmem + lane_base + C::tS(s);
+      const uint32_t tO = tmem + lane_base + C::tO(s);
+      const uint32_t tP = tmem + lane_base + C::tP(s);
       const int qp = qp0 + row;                // this row's query position
       const float sl2 = a.scale * 1.4426950408889634f;
       float m_ref = -INFINITY, l = 0.f;
-      uint8_t* sP = smem + C::kOffP + s * C::kPBytes;
-      const uint32_t sP_u32 = smem_u32(sP);
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&bars->s_full[s], j & 1);
         tc_fence_after();
@@ -201,8 +207,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[c + i] = __uint_as_float(r[i]);
         }
-        tc_fence_before();
-        mbar_arrive(&bars->s_free[s]);        // S_s TMEM may now take S_s(j+1)
+        if (!C::kPAlias) {
+          tc_fence_before();
+          mbar_arrive(&bars->s_free[s]);      // S_s TMEM may now take S_s(j+1)
+        }
         const int kv0 = j * BN;
         if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
 #pragma unroll
@@ -246,21 +254,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};               // 4 independent row-sum chains
 #pragma unroll
-        for (int c = 0; c < BN; c += 8) {
-          float pv[8];
+        for (int c0 = 0; c0 < BN; c0 += 64) {
+          uint32_t pk[32];                                 // 64 P values as bf16 pairs
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float xx = fmaf(x[c + i], sl2, neg_m);
-            // 3 of every 8 exponentials on the FMA pipe, 5 on MUFU (MUFU ex2 is the d=64 bound)
-            pv[i] = (i % 8) < kPolyPer8 ? ex2_poly(xx) : ex2(xx);
-            ls[i % 4] += pv[i];
+          for (int c = c0; c < c0 + 64; c += 8) {
+            float pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float xx = fmaf(x[c + i], sl2, neg_m);
+              // some exponentials on the FMA pipe, the rest on MUFU (MUFU ex2 is the d=64 bound)
+              pv[i] = (i % 8) < kPolyPer8 ? ex2_poly(xx) : ex2(xx);
+              ls[i % 4] += pv[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pk[(c - c0) / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
           }
-          const uint32_t addr = sP_u32 + (c / 64) * (BM * 128) + sw128_off(row, c % 64);
-          st_shared_v4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
-                       pack_bf16(pv[6], pv[7]));
+          tmem_st32(tP + c0 / 2, pk);
         }
         l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-        fence_async_smem();
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
       }

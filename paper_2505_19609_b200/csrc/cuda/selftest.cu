@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_init(bar_mma, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
   // variant 3: A [128][128] written by threads into SW128 K-major smem (as P is in attention)
   if (variant == 3) {
     const int row = threadIdx.x;
@@ -39,9 +39,23 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // variant 4: A [128][128] written by threads into TMEM columns [128, 192) as packed bf16 pairs
+  if (variant == 4) {
+    const int row = threadIdx.x;
+    for (int c = 0; c < 64; c += 32) {
+      uint32_t r[32];
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(A + row * 128 + 2 * c);
+      for (int i = 0; i < 32; ++i) r[i] = src[i];
+      tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + 128 + c, r);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   if (threadIdx.x == 0) {
-    const bool a_tma = variant != 3;
+    const bool a_tma = variant != 3 && variant != 4;
     const bool b_mn = variant == 1 || variant == 2;
     const bool a_mn = variant == 2;
     uint32_t bytes = (a_tma ? 32768u : 0u) + (b_mn ? (uint32_t)n * 256u : (uint32_t)n * 256u);
@@ -69,7 +83,10 @@ __global__ void __launch_bounds__(128, 1)
         bd = sdesc_sw128(smem_u32(sB) + k * 2048, 16384, 1024);
       else
         bd = sdesc_sw128(smem_u32(sB) + (k / 4) * (n * 128) + (k % 4) * 32, 16, 1024);
-      umma_f16(tmem, ad, bd, idesc, k > 0);
+      if (variant == 4)
+        umma_f16_ts(tmem, tmem + 128 + k * 8, bd, idesc, k > 0);
+      else
+        umma_f16(tmem, ad, bd, idesc, k > 0);
     }
     umma_commit(bar_mma);
   }
@@ -85,7 +102,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<128>(tmem);
+  if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace skr
@@ -94,7 +111,7 @@ SKR_EXPORT skr_status skr_selftest_umma(int32_t variant, int32_t n, const void* 
                                          void* stream) {
   using namespace skr;
   if (skr_status s = check_sm100()) return s;
-  SKR_REQUIRE(variant >= 0 && variant <= 3 && (n == 64 || n == 128) && A && B && C, "bad selftest args");
+  SKR_REQUIRE(variant >= 0 && variant <= 4 && (n == 64 || n == 128) && A && B && C, "bad selftest args");
   CUtensorMap ta, tb;
   const bool b_mn = variant == 1 || variant == 2;
   // A: K-major [128][128] (variants 0,1) or MN-major given as [K=128][M=128] (variant 2): same shape.

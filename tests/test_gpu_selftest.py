@@ -7,7 +7,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("n", [64, 128])
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_umma_layouts(variant, n):
     from paper_2505_19609_b200 import skrull
     g = torch.Generator(device="cuda").manual_seed(variant * 7 + n)
@@ -20,7 +20,7 @@ def test_umma_layouts(variant, n):
     skrull.skr_selftest_umma(variant, n, A, B, C)
     torch.cuda.synchronize()
     Af, Bf = A.float(), B.float()
-    if variant == 0 or variant == 3:
+    if variant in (0, 3, 4):
         ref = Af @ Bf.T
     elif variant == 1:
         ref = Af @ Bf
