@@ -15,6 +15,8 @@
 // into TMEM with tcgen05.st and fed to the PV MMA as its A operand straight from TMEM (no smem
 // traffic: with single-CTA M=128 MMAs the SS operand reads alone saturate shared memory). Causal: only KV tiles up to the tile's last
 // query are visited (bottom-right aligned with q_pos, R23); the diagonal tiles are masked.
+#include <cstdlib>
+
 #include "attn_common.cuh"
 #include "device.cuh"
 #include "sm100.cuh"
@@ -26,7 +28,6 @@ namespace fwd {
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr int kPolyPer8 = 3;               // exponentials per 8 computed by ex2_poly
 
 template <int D>
 struct Cfg {
@@ -54,8 +55,8 @@ struct Bars {  // kUnits <= 8
   uint32_t tmem_base;
 };
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, int kPolyPer8>   // kPolyPer8: exponentials per 8 computed by ex2_poly on the FMA pipe
+__global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (16K regs) -> <= 168 regs
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, int pairs_per_group) {
@@ -149,37 +150,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       mbar_wait(&bars->q_full, 0);
       tc_fence_after();
-      // KV units arrive in the order K0 V0 K1 V1 ...; S(j+1) is issued as soon as the softmax has read
-      // S(j) out of TMEM (s_free), so it overlaps the exponentials of tile j; PV(j) after P(j).
-      mbar_wait(&bars->kv_full[0], 0);
-      tc_fence_after();
-      for (int s = 0; s < nq; ++s) issue_s(s, sKV);
-      umma_commit(&bars->kv_empty[0]);
-      for (int j = 0; j < n_kv; ++j) {
-        const int itv = 2 * j + 1, itk = 2 * j + 2;      // ring positions of V(j) and K(j+1)
-        const bool more = j + 1 < n_kv;
-        const int uk = itk % C::kUnits, uv = itv % C::kUnits;
-        if (!C::kPAlias && more) {
-          // separate P columns: S(j+1) as soon as the softmax has read S(j)
-          mbar_wait(&bars->kv_full[uk], (itk / C::kUnits) & 1);
-          for (int s = 0; s < nq; ++s) {
-            mbar_wait(&bars->s_free[s], j & 1);
-            tc_fence_after();
-            issue_s(s, sKV + uk * C::kKVBytes);
+      // Event-driven issue: K/V units arrive in ring order K0 V0 K1 V1 ...; each head s has a next S
+      // tile js[s] and a next PV tile jp[s]; whatever is ready is issued (non-blocking probes), so one
+      // head never waits behind the other's barriers. S_s(j) needs K(j) and its S columns free
+      // (separate P: the softmax read S_s(j-1), s_free; P aliasing S: PV_s(j-1) issued before it in
+      // the in-order tensor pipe). PV_s(j) needs V(j) and P_s(j) (p_full). A K / V unit is released
+      // once every head has issued the MMAs that read it.
+      int js[2] = {0, 0}, jp[2] = {0, nq > 1 ? 0 : n_kv};
+      if (nq == 1) js[1] = n_kv;
+      int kfree = 0, vfree = 0;
+      while (jp[0] < n_kv || jp[1] < n_kv) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int j = js[s];
+          if (j < n_kv) {
+            const int itk = 2 * j, uk = itk % C::kUnits;
+            bool ok = mbar_test(&bars->kv_full[uk], (itk / C::kUnits) & 1);
+            if (ok && j > 0) ok = C::kPAlias ? jp[s] >= j : mbar_test(&bars->s_free[s], (j - 1) & 1);
+            if (ok) {
+              tc_fence_after();
+              issue_s(s, sKV + uk * C::kKVBytes);
+              js[s] = j + 1;
+            }
           }
-          umma_commit(&bars->kv_empty[uk]);
+          const int jv = jp[s];
+          if (jv < js[s]) {
+            const int itv = 2 * jv + 1, uv = itv % C::kUnits;
+            if (mbar_test(&bars->kv_full[uv], (itv / C::kUnits) & 1) && mbar_test(&bars->p_full[s], jv & 1)) {
+              tc_fence_after();
+              issue_pv(s, sKV + uv * C::kKVBytes, jv > 0);
+              jp[s] = jv + 1;
+            }
+          }
         }
-        mbar_wait(&bars->kv_full[uv], (itv / C::kUnits) & 1);
-        if (C::kPAlias && more) mbar_wait(&bars->kv_full[uk], (itk / C::kUnits) & 1);
-        for (int s = 0; s < nq; ++s) {
-          mbar_wait(&bars->p_full[s], j & 1);            // P_s(j) in TMEM, O_s corrected
-          tc_fence_after();
-          issue_pv(s, sKV + uv * C::kKVBytes, j > 0);
-          // P aliases S: S(j+1) enters the (in-order) tensor pipe after PV(j) has read P(j)
-          if (C::kPAlias && more) issue_s(s, sKV + uk * C::kKVBytes);
-        }
-        umma_commit(&bars->kv_empty[uv]);
-        if (C::kPAlias && more) umma_commit(&bars->kv_empty[uk]);
+        for (; kfree < min(js[0], js[1]); ++kfree) umma_commit(&bars->kv_empty[(2 * kfree) % C::kUnits]);
+        for (; vfree < min(jp[0], jp[1]); ++vfree) umma_commit(&bars->kv_empty[(2 * vfree + 1) % C::kUnits]);
       }
     }
   } else {
@@ -226,52 +231,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
                                fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
         const float m_new = fmaxf(m_ref, mx * sl2);
-        // P_s(j-1) consumed and O_s(j-1) accumulated before P / O are touched again
+        // tcgen05.ld/st are warp-collective: the rescale decision is made per warp (every lane of
+        // the warp moves its reference max to its own m_new; alpha == 1 where nothing changed)
+        const bool rescale = __any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0;
+        const float alpha = (rescale && j > 0) ? ex2(m_ref - m_new) : 1.f;
+        if (rescale) m_ref = m_new;
+        // P = exp2(S * scale * log2e - m_ref) into registers (bf16 pairs) before waiting for PV(j-1),
+        // so the PV MMA has the whole exponential phase to complete.
+        const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};               // 4 independent row-sum chains
+        uint32_t pk[BN / 2];
+#pragma unroll
+        for (int c = 0; c < BN; c += 8) {
+          float pv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float xx = fmaf(x[c + i], sl2, neg_m);
+            // some exponentials on the FMA pipe, the rest on MUFU (MUFU ex2 is the d=64 bound)
+            pv[i] = (i % 8) < kPolyPer8 ? ex2_poly(xx) : ex2(xx);
+            ls[i % 4] += pv[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
+        }
+        // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
         if (j > 0) {
           mbar_wait(&bars->pv_done[s], (j - 1) & 1);
           tc_fence_after();
         }
-        // tcgen05.ld/st are warp-collective: the rescale decision is made per warp (every lane of
-        // the warp moves its reference max to its own m_new; alpha == 1 where nothing changed)
-        if (__any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0) {
-          const float alpha = j == 0 ? 0.f : ex2(m_ref - m_new);
-          if (j > 0) {
+        if (rescale && j > 0) {
 #pragma unroll
-            for (int c = 0; c < D; c += 16) {
-              uint32_t r[16];
-              tmem_ld16(tO + c, r);
-              tmem_wait_ld();
+          for (int c = 0; c < D; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(tO + c, r);
+            tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tmem_st16(tO + c, r);
-            }
-            tmem_wait_st();
+            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st16(tO + c, r);
           }
-          l *= alpha;
-          m_ref = m_new;
         }
-        // P = exp2(S * scale * log2e - m_ref), row sum, bf16 into swizzled smem (K-major A operand)
-        const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};               // 4 independent row-sum chains
+        l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 64) {
-          uint32_t pk[32];                                 // 64 P values as bf16 pairs
+        for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+          uint32_t q[32];
 #pragma unroll
-          for (int c = c0; c < c0 + 64; c += 8) {
-            float pv[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float xx = fmaf(x[c + i], sl2, neg_m);
-              // some exponentials on the FMA pipe, the rest on MUFU (MUFU ex2 is the d=64 bound)
-              pv[i] = (i % 8) < kPolyPer8 ? ex2_poly(xx) : ex2(xx);
-              ls[i % 4] += pv[i];
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) pk[(c - c0) / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
-          }
-          tmem_st32(tP + c0 / 2, pk);
+          for (int i = 0; i < 32; ++i) q[i] = pk[c0 + i];
+          tmem_st32(tP + c0, q);
         }
-        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
@@ -321,14 +327,33 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   const int grp = a.hq / a.hkv;
   const int ppg = (grp + 1) / 2;
   dim3 grid(a.hkv * ppg, a.n_tiles);
+  // share of exponentials on the FMA pipe (MUFU ex2 bounds the d = 64 forward); SKR_FWD_POLY overrides
+  static int poly = [] {
+    const char* e = getenv("SKR_FWD_POLY");
+    const int v = e ? atoi(e) : -1;
+    return (v >= 0 && v <= 3) ? v : -1;
+  }();
+  const int pp = poly >= 0 ? poly : (d == 64 ? 1 : 0);   // measured: more poly only adds issue pressure
+  auto launch = [&](auto kern, int smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
+  };
   if (d == 128) {
     constexpr int smem = fwd::Cfg<128>::kSmem;
-    cudaFuncSetAttribute(fwd::attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    fwd::attn_fwd_kernel<128><<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
+    switch (pp) {
+      case 0: launch(fwd::attn_fwd_kernel<128, 0>, smem); break;
+      case 1: launch(fwd::attn_fwd_kernel<128, 1>, smem); break;
+      case 2: launch(fwd::attn_fwd_kernel<128, 2>, smem); break;
+      default: launch(fwd::attn_fwd_kernel<128, 3>, smem); break;
+    }
   } else if (d == 64) {
     constexpr int smem = fwd::Cfg<64>::kSmem;
-    cudaFuncSetAttribute(fwd::attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    fwd::attn_fwd_kernel<64><<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
+    switch (pp) {
+      case 0: launch(fwd::attn_fwd_kernel<64, 0>, smem); break;
+      case 1: launch(fwd::attn_fwd_kernel<64, 1>, smem); break;
+      case 2: launch(fwd::attn_fwd_kernel<64, 2>, smem); break;
+      default: launch(fwd::attn_fwd_kernel<64, 3>, smem); break;
+    }
   } else {
     return fail(SKR_E_UNSUPPORTED, "bf16 attention supports d in {64, 128}");
   }
