@@ -143,26 +143,42 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def ncu_traffic(workload, world, kind):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed `ncu --set full`
+    capture summary (profiles/ncu_summary.json, written by profiles/summarize_ncu.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        e = j[f"{workload}/n{world}"][f"attn_{kind}"]
+        return {"bytes_per_launch": e["dram_bytes"], "launches_per_step": e.get("launches_per_step"),
+                "source": e.get("source", "profiles/ncu_summary.json")}
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 def cpu_oracle_sample(lens, shape: Shape, seconds: float, seed: int = 0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: sequences taken
-    shortest-first until `seconds` of CPU work. Returns (TFLOP/s, n_seqs, tokens, wall_s)."""
+    shortest-first while the projected time (measured FLOP rate so far x the next sequence's useful
+    FLOPs) stays within `seconds`. Returns (TFLOP/s, n_seqs, tokens, wall_s)."""
     from oracle.attention import attn_bwd, attn_fwd
     from synth import seq_tensors
     order = np.argsort(lens, kind="stable")
     done_flops, n, toks, t_used = 0, 0, 0, 0.0
     for k in order:
         S = int(lens[k])
+        f = useful_flops([S], shape)
+        if n > 0 and t_used + f / (done_flops / t_used) > seconds:
+            break
         x = seq_tensors(seed, int(k), S, shape.hq, shape.hkv, shape.d)
         t0 = time.perf_counter()
         attn_fwd(x["q"], x["k"], x["v"])
         attn_bwd(x["q"], x["k"], x["v"], x["do"])
         t_used += time.perf_counter() - t0
-        done_flops += useful_flops([S], shape)
+        done_flops += f
         n += 1
         toks += S
-        if t_used >= seconds:
-            break
     return done_flops / t_used / 1e12, n, toks, t_used
 
 
@@ -237,21 +253,10 @@ def run_ours(args):
                for k, hh in (("q", shp.hq), ("k", shp.hkv), ("v", shp.hkv), ("do", shp.hq))}
         steps.append((rs, src))
 
-    fwd_ev, bwd_ev = [], []
-
-    def one_step(record=False):
+    def one_step():
         for rs, src in steps:
-            if record:
-                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-                e0.record()
             rs.forward(src["q"], src["k"], src["v"], comm, side)
-            if record:
-                e1.record()
             rs.backward(src["do"], comm, side)
-            if record:
-                e2.record()
-                fwd_ev.append((e0, e1))
-                bwd_ev.append((e1, e2))
 
     def barrier():
         if world > 1:
@@ -276,14 +281,20 @@ def run_ours(args):
     clocks = clk.stop()
     my_ms = start.elapsed_time(end) / args.steps
 
-    # per-phase timing pass (separate from the headline timing; events around fwd / bwd)
-    fwd_ev.clear(), bwd_ev.clear()
-    for _ in range(max(2, min(args.steps, 5))):
-        one_step(record=True)
-    torch.cuda.synchronize()
+    # per-kernel timing pass (separate from the headline timing): CUDA events on the launching
+    # stream around every attention fwd / bwd C-ABI call
     nrep = max(2, min(args.steps, 5))
-    fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / nrep
-    bwd_ms = sum(a.elapsed_time(b) for a, b in bwd_ev) / nrep
+    for rs, _ in steps:
+        rs.events = []
+    for _ in range(nrep):
+        one_step()
+    torch.cuda.synchronize()
+    kt = {"fwd": 0.0, "bwd": 0.0}
+    for rs, _ in steps:
+        for kind, a, b in rs.events:
+            kt[kind] += a.elapsed_time(b)
+        rs.events = None
+    fwd_ms, bwd_ms = kt["fwd"] / nrep, kt["bwd"] / nrep
 
     # ---- e2e: host pinned inputs -> device, step, gradients back to host
     e2e = None
@@ -336,6 +347,7 @@ def run_ours(args):
         fwd_fl, bwd_fl = 4 * shp.d * shp.hq * my_pairs, 10 * shp.d * shp.hq * my_pairs
         dom = ("bwd", bwd_fl, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", fwd_fl, fwd_ms)
         achieved = dom[1] / (dom[2] * 1e-3) / 1e12
+        traffic = ncu_traffic(name, world, dom[0])
         peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
         gpu_launches = args.steps * sum(rs.launches_per_step() for rs, _ in steps)
         cpu = None
@@ -358,7 +370,7 @@ def run_ours(args):
                        "rollbacks": int(plan["n_rollbacks"]),
                        "l2": "inputs larger than L2 (no flush)", "parallelism": f"cp{cp}"},
             "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]}", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{which} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
             "cpu_baseline": cpu,
             "e2e": None if e2e is None else {"value": total_flops / (float(allv[:, 3].max()) * 1e-3) / 1e12,

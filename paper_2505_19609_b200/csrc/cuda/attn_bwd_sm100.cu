@@ -17,6 +17,8 @@
 // dQ accumulator), warp 12 TMA producer (K, V once; Q/dO ring of 2 + LSE/D rows), warp 13 MMA.
 // MMA order per step n: S(n+1) as soon as S(n) is read | dV(n) after P(n) | dP(n+1) as soon as dP(n)
 // is read | dK(n) dQ(n) after dS(n): the tensor core runs ahead while the compute warpgroups work.
+#include <cstdlib>
+
 #include "attn_common.cuh"
 #include "device.cuh"
 #include "sm100.cuh"
@@ -24,6 +26,16 @@
 
 namespace skr {
 namespace bwd {
+
+// Debug timeline (SKR_TRACE=1): (event, clock) pairs of block (0, 0) into a device buffer.
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned int g_trace_n = 0;
+__device__ __forceinline__ void trace(int ev) {
+  if (g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
+    const unsigned int i = atomicAdd(&g_trace_n, 1u);
+    if (i < 8192) g_trace[i] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+  }
+}
 
 constexpr int BN = 128;  // key tile
 constexpr int kThreads = 448;
@@ -129,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 12) {
     // ================= TMA producer (+ LSE / D rows of each step into smem)
-    if (lane == 0) {
+    if (elect_one()) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
@@ -161,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int st = n % C::kStages;
       const int h = g * grp + it.hi, q0 = it.qt * BQ;
       mbar_wait(&bars->qdo_empty[st], ((n / C::kStages) & 1) ^ 1);
-      if (lane == 0) {
+      if (elect_one()) {
         mbar_expect_tx(&bars->qdo_full[st], 2 * C::kQBytes);
         for (int c = 0; c < C::kChunks; ++c) {
           tma_load_2d(smem + C::kOffQ + st * C::kQBytes + c * BQ * 128, &tm_q, &bars->qdo_full[st], h * D + c * 64,
@@ -181,91 +193,116 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (n + 1 < n_steps) fetch(it);
     }
   } else if (warp == 13) {
-    // ================= MMA issuer
-    if (lane == 0) {
-      const uint32_t sK = smem_u32(smem + C::kOffK), sV = smem_u32(smem + C::kOffV);
-      const uint32_t sQ = smem_u32(smem + C::kOffQ), sDO = smem_u32(smem + C::kOffDO);
-      const uint32_t sDS = smem_u32(smem + C::kOffDS);
-      const uint32_t id_sdp = idesc_bf16_f32(BN, BQ, 0, 0);   // S^T = K Q^T, dP^T = V dO^T
-      const uint32_t id_kv = idesc_bf16_f32(BN, D, 0, 1);     // dV += P^T dO, dK += dS^T Q
-      // dQ^T = K^T dS^T (d = 128) or dQ = dS K (d = 64): both operands MN-major
-      const uint32_t id_dq = D == 128 ? idesc_bf16_f32(D, BQ, 1, 1) : idesc_bf16_f32(BQ, D, 1, 1);
-      auto issue_t = [&](uint32_t a_base, uint32_t b_base, uint32_t tcol) {
+    // ================= MMA issuer: warp-converged control flow, one elected lane issues each group
+    // (issuing from a divergent lane makes every tcgen05.mma an ELECT/R2UR waterfall, ~100 cycles).
+    const uint32_t sK = smem_u32(smem + C::kOffK), sV = smem_u32(smem + C::kOffV);
+    const uint32_t sQ = smem_u32(smem + C::kOffQ), sDO = smem_u32(smem + C::kOffDO);
+    const uint32_t sDS = smem_u32(smem + C::kOffDS);
+    const uint32_t id_sdp = idesc_bf16_f32(BN, BQ, 0, 0);   // S^T = K Q^T, dP^T = V dO^T
+    const uint32_t id_kv = idesc_bf16_f32(BN, D, 0, 1);     // dV += P^T dO, dK += dS^T Q
+    // dQ^T = K^T dS^T (d = 128) or dQ = dS K (d = 64): both operands MN-major
+    const uint32_t id_dq = D == 128 ? idesc_bf16_f32(D, BQ, 1, 1) : idesc_bf16_f32(BQ, D, 1, 1);
+    // descriptor of (base + off) == descriptor of base + (off >> 4)
+    const uint64_t dK = sdesc_sw128(sK, 16, 1024), dV = sdesc_sw128(sV, 16, 1024);
+    const uint64_t dQ = sdesc_sw128(sQ, 16, 1024), dDO = sdesc_sw128(sDO, 16, 1024);
+    const uint64_t dQmn = sdesc_sw128(sQ, BQ * 128, 1024), dDOmn = sdesc_sw128(sDO, BQ * 128, 1024);
+    const uint64_t dKmn = sdesc_sw128(sK, BN * 128, 1024), dDSmn = sdesc_sw128(sDS, BN * 128, 1024);
+    const uint64_t dK0 = sdesc_sw128(sK, 0, 1024), dDS0 = sdesc_sw128(sDS, 0, 1024);
+    auto issue_t = [&](uint64_t a_desc, uint64_t b_desc, uint32_t tcol) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t ao = (k / 4) * (BN * 128) + (k % 4) * 32;
-          const uint32_t bo = (k / 4) * (BQ * 128) + (k % 4) * 32;
-          umma_f16(tmem + tcol, sdesc_sw128(a_base + ao, 16, 1024), sdesc_sw128(b_base + bo, 16, 1024), id_sdp,
-                   k > 0);
-        }
-      };
-      // dV / dK: A = P^T or dS^T from TMEM (k-step = 16 queries = 8 packed columns of one warpgroup
-      // half), B = dO or Q tile (MN-major over d)
-      auto issue_kv = [&](bool is_dk, uint32_t b_base, uint32_t tcol, bool acc) {
+      for (int k = 0; k < D / 16; ++k) {
+        const uint32_t ao = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
+        const uint32_t bo = ((k / 4) * (BQ * 128) + (k % 4) * 32) >> 4;
+        umma_f16(tmem + tcol, a_desc + ao, b_desc + bo, id_sdp, k > 0);
+      }
+    };
+    // dV / dK: A = P^T or dS^T from TMEM (k-step = 16 queries = 8 packed columns of one warpgroup
+    // half), B = dO or Q tile (MN-major over d)
+    auto issue_kv = [&](bool is_dk, uint64_t b_desc, uint32_t tcol, bool acc) {
 #pragma unroll
-        for (int k = 0; k < BQ / 16; ++k) {
-          const int w = (k * 16) / H, kk = (k * 16) % H;
-          const uint32_t a_col = (is_dk ? C::tDS(w) : C::tPTw(w)) + kk / 2;
-          umma_f16_ts(tmem + tcol, tmem + a_col, sdesc_sw128(b_base + k * 2048, BQ * 128, 1024), id_kv, acc || k > 0);
-        }
-      };
-      auto issue_dq = [&]() {
+      for (int k = 0; k < BQ / 16; ++k) {
+        const int w = (k * 16) / H, kk = (k * 16) % H;
+        const uint32_t a_col = (is_dk ? C::tDS(w) : C::tPTw(w)) + kk / 2;
+        umma_f16_ts(tmem + tcol, tmem + a_col, b_desc + ((uint32_t)(k * 2048) >> 4), id_kv, acc || k > 0);
+      }
+    };
+    auto issue_dq = [&]() {
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) {
-          if (D == 128)
-            umma_f16(tmem + C::tDQ, sdesc_sw128(sK + k * 2048, BN * 128, 1024), sdesc_sw128(sDS + k * 2048, 0, 1024),
-                     id_dq, k > 0);
-          else
-            umma_f16(tmem + C::tDQ, sdesc_sw128(sDS + k * 2048, BN * 128, 1024), sdesc_sw128(sK + k * 2048, 0, 1024),
-                     id_dq, k > 0);
-        }
-      };
-      mbar_wait(&bars->kv_full, 0);
-      mbar_wait(&bars->qdo_full[0], 0);
-      tc_fence_after();
-      issue_t(sK, sQ, C::tS);
+      for (int k = 0; k < BN / 16; ++k) {
+        const uint32_t o = (uint32_t)(k * 2048) >> 4;
+        if (D == 128)
+          umma_f16(tmem + C::tDQ, dKmn + o, dDS0 + o, id_dq, k > 0);
+        else
+          umma_f16(tmem + C::tDQ, dDSmn + o, dK0 + o, id_dq, k > 0);
+      }
+    };
+    const uint32_t qstage = (uint32_t)C::kQBytes >> 4;
+    mbar_wait(&bars->kv_full, 0);
+    mbar_wait(&bars->qdo_full[0], 0);
+    tc_fence_after();
+    if (elect_one()) {
+      issue_t(dK, dQ, C::tS);
       umma_commit(&bars->s_full);
-      issue_t(sV, sDO, C::tDP);
+      issue_t(dV, dDO, C::tDP);
       umma_commit(&bars->dp_full);
-      // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its own
-      // columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows dK(n)
-      // in the in-order tensor pipe.
-      for (int n = 0; n < n_steps; ++n) {
-        const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
-        const bool more = n + 1 < n_steps;
-        mbar_wait(&bars->s_free, n & 1);
-        if (more) {
-          mbar_wait(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
-          tc_fence_after();
-          issue_t(sK, sQ + st1 * C::kQBytes, C::tS);
+    }
+    __syncwarp();
+    // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its own
+    // columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows dK(n)
+    // in the in-order tensor pipe.
+    for (int n = 0; n < n_steps; ++n) {
+      const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
+      const bool more = n + 1 < n_steps;
+      mbar_wait(&bars->s_free, n & 1);
+      trace(1);
+      if (more) {
+        mbar_wait(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
+        trace(2);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_t(dK, dQ + st1 * qstage, C::tS);
           umma_commit(&bars->s_full);
         }
-        mbar_wait(&bars->p_full, n & 1);
-        tc_fence_after();
-        issue_kv(false, sDO + st * C::kQBytes, C::tDV, n > 0);
+        __syncwarp();
+      }
+      mbar_wait(&bars->p_full, n & 1);
+      trace(3);
+      tc_fence_after();
+      if (elect_one()) {
+        issue_kv(false, dDOmn + st * qstage, C::tDV, n > 0);
         umma_commit(&bars->dv_done);
-        if (!C::kDSAlias) {
-          mbar_wait(&bars->dp_free, n & 1);
-          if (more) {
-            tc_fence_after();
-            issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
+      }
+      __syncwarp();
+      if (!C::kDSAlias) {
+        mbar_wait(&bars->dp_free, n & 1);
+        if (more) {
+          tc_fence_after();
+          if (elect_one()) {
+            issue_t(dV, dDO + st1 * qstage, C::tDP);
             umma_commit(&bars->dp_full);
           }
+          __syncwarp();
         }
-        mbar_wait(&bars->ds_full, n & 1);
-        tc_fence_after();
-        issue_kv(true, sQ + st * C::kQBytes, C::tDK, n > 0);
-        mbar_wait(&bars->dq_empty, (n & 1) ^ 1);
-        tc_fence_after();
+      }
+      mbar_wait(&bars->ds_full, n & 1);
+      trace(4);
+      tc_fence_after();
+      if (elect_one()) issue_kv(true, dQmn + st * qstage, C::tDK, n > 0);
+      __syncwarp();
+      mbar_wait(&bars->dq_empty, (n & 1) ^ 1);
+      trace(5);
+      tc_fence_after();
+      if (elect_one()) {
         issue_dq();
         umma_commit(&bars->dq_full);
         umma_commit(&bars->dsq_done);
         umma_commit(&bars->qdo_empty[st]);
         if (C::kDSAlias && more) {
-          issue_t(sV, sDO + st1 * C::kQBytes, C::tDP);
+          issue_t(dV, dDO + st1 * qstage, C::tDP);
           umma_commit(&bars->dp_full);
         }
       }
+      __syncwarp();
     }
   } else if (warp < 8) {
     // ================= two compute warpgroups: thread = key row, warpgroup = half of the query columns
@@ -285,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1);
       const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (C::kStages * BQ + st * BQ + col0) * 4;
       mbar_wait(&bars->s_full, n & 1);
+      if (threadIdx.x == 0) trace(10);
       tc_fence_after();
       float p[H];
 #pragma unroll
@@ -321,7 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
+      if (threadIdx.x == 0) trace(11);
       mbar_wait(&bars->dp_full, n & 1);
+      if (threadIdx.x == 0) trace(12);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < H; c += 32) {
@@ -359,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->ds_full);
+      if (threadIdx.x == 0) trace(13);
     }
     // ---- dK, dV epilogue: warpgroup 0 stores dK, warpgroup 1 stores dV
     mbar_wait(&bars->dsq_done, (n_steps - 1) & 1);
@@ -404,9 +445,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int n = 0; n < n_steps; ++n, it.next()) {
       const int h = g * grp + it.hi, q0 = it.qt * BQ;
       mbar_wait(&bars->dq_full, n & 1);
+      if (t == 0) trace(20);
       tc_fence_after();
       // the previous step's reduce must have finished reading the smem tile
-      if (t == 0) bulk_wait_read<0>();
+      if (warp == 8 && elect_one()) bulk_wait_read<0>();
       named_bar_sync(1, 128);
       if (D == 128) {
         // dQ^T: lane = feature t, columns = queries of the step
@@ -435,15 +477,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars->dq_empty);                // TMEM dQ columns may be overwritten
+      if (t == 0) trace(21);
       fence_async_smem();
       named_bar_sync(1, 128);
-      if (t == 0) {
+      if (warp == 8) {
+        if (elect_one()) {
 #pragma unroll
-        for (int b = 0; b < kBoxes; ++b) tma_reduce_add_2d(&tm_dq, smem + C::kOffDQ + b * kBoxBytes, h * D + b * 32, cu0 + q0);
-        bulk_commit();
+          for (int b = 0; b < kBoxes; ++b)
+            tma_reduce_add_2d(&tm_dq, smem + C::kOffDQ + b * kBoxBytes, h * D + b * 32, cu0 + q0);
+          bulk_commit();
+        }
+        __syncwarp();
       }
     }
-    if (t == 0) bulk_wait<0>();
+    if (warp == 8 && elect_one()) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -500,10 +547,38 @@ __global__ void convert_dq_kernel(const float4* __restrict__ acc, uint2* __restr
 
 }  // namespace bwd
 
+static unsigned long long* trace_buffer() {
+  static unsigned long long* buf = nullptr;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    if (getenv("SKR_TRACE")) {
+      cudaMalloc(&buf, 8192 * sizeof(unsigned long long));
+      cudaMemcpyToSymbol(bwd::g_trace, &buf, sizeof(buf));
+    }
+  }
+  return buf;
+}
+
+// Debug aid: copy the last bwd trace (event << 48 | clock) to host; returns the number of entries.
+extern "C" __attribute__((visibility("default"))) int skr_debug_bwd_trace(unsigned long long* out, int cap) {
+  unsigned long long* buf = trace_buffer();
+  if (!buf) return 0;
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, bwd::g_trace_n, sizeof(n));
+  n = n > 8192 ? 8192 : n;
+  n = (int)n > cap ? cap : n;
+  cudaMemcpy(out, buf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  unsigned int z = 0;
+  cudaMemcpyToSymbol(bwd::g_trace_n, &z, sizeof(z));
+  return (int)n;
+}
+
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
                           const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
                           void* dv, int accumulate, float* Dbuf, float* dq_acc, int n_q_rows, int n_kv_rows,
                           cudaStream_t st) {
+  trace_buffer();
   if (d != 64 && d != 128) return fail(SKR_E_UNSUPPORTED, "bf16 backward supports d in {64,128}");
   const int rows = row_end - row_begin;
   if (rows > 0) {

@@ -100,8 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
   const uint32_t tmem = bars->tmem_base;
 
   if (warp == 8) {
-    // ================= TMA producer
-    if (lane == 0) {
+    // ================= TMA producer (warp-converged loop, one elected lane issues)
+    if (elect_one()) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
@@ -111,80 +111,95 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_2d(smem + C::kOffQ + s * C::kQBytes + c * (BM * 128), &tm_q, &bars->q_full, h * D + c * 64, r0);
       }
-      int it = 0;
-      for (int j = 0; j < n_kv; ++j) {
-        for (int kv = 0; kv < 2; ++kv, ++it) {
-          const int u = it % C::kUnits;
-          mbar_wait(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+    }
+    __syncwarp();
+    int it = 0;
+    for (int j = 0; j < n_kv; ++j) {
+      for (int kv = 0; kv < 2; ++kv, ++it) {
+        const int u = it % C::kUnits;
+        mbar_wait(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(&bars->kv_full[u], C::kKVBytes);
           uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
           for (int c = 0; c < C::kChunks; ++c)
             tma_load_2d(dst + c * (BN * 128), kv == 0 ? &tm_k : &tm_v, &bars->kv_full[u], g * D + c * 64,
                         kst + j * BN);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 9) {
-    // ================= MMA issuer
-    if (lane == 0) {
-      const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0);   // S = Q K^T   (both K-major)
-      const uint32_t id_o = idesc_bf16_f32(BM, D, 0, 1);    // O += P V    (V is MN-major)
-      const uint32_t sQ = smem_u32(smem + C::kOffQ), sKV = smem_u32(smem + C::kOffKV);
-      auto issue_s = [&](int s, uint32_t k_addr) {
-        const uint32_t q_addr = sQ + s * C::kQBytes;
+    // ================= MMA issuer: the warp runs the control flow converged (descriptors stay
+    // warp-uniform, no per-instruction ELECT/R2UR waterfall); one elected lane issues each MMA group.
+    const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0);   // S = Q K^T   (both K-major)
+    const uint32_t id_o = idesc_bf16_f32(BM, D, 0, 1);    // O += P V    (V is MN-major)
+    const uint32_t sQ = smem_u32(smem + C::kOffQ), sKV = smem_u32(smem + C::kOffKV);
+    // descriptor of (base + off) == descriptor of base + (off >> 4): the start address is the low field
+    const uint64_t dq0 = sdesc_sw128(sQ, 16, 1024), dkv0 = sdesc_sw128(sKV, 16, 1024);
+    const uint64_t dv0 = sdesc_sw128(sKV, BN * 128, 1024);
+    auto issue_s = [&](int s, int u) {
+      const uint64_t dq = dq0 + ((uint32_t)(s * C::kQBytes) >> 4), dk = dkv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * (BM * 128) + (k % 4) * 32;
-          const uint32_t koff = (k / 4) * (BN * 128) + (k % 4) * 32;
-          umma_f16(tmem + C::tS(s), sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + koff, 16, 1024), id_s,
-                   k > 0);
-        }
-        umma_commit(&bars->s_full[s]);
-      };
-      auto issue_pv = [&](int s, uint32_t v_addr, bool acc) {
+      for (int k = 0; k < D / 16; ++k) {
+        const uint32_t off = ((k / 4) * (BM * 128) + (k % 4) * 32) >> 4;
+        const uint32_t koff = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
+        umma_f16(tmem + C::tS(s), dq + off, dk + koff, id_s, k > 0);
+      }
+      umma_commit(&bars->s_full[s]);
+    };
+    auto issue_pv = [&](int s, int u, bool acc) {
+      const uint64_t dv = dv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k)
-          umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, sdesc_sw128(v_addr + k * 2048, BN * 128, 1024), id_o,
-                      acc || k > 0);
-        umma_commit(&bars->pv_done[s]);
-      };
-      mbar_wait(&bars->q_full, 0);
-      tc_fence_after();
-      // Event-driven issue: K/V units arrive in ring order K0 V0 K1 V1 ...; each head s has a next S
-      // tile js[s] and a next PV tile jp[s]; whatever is ready is issued (non-blocking probes), so one
-      // head never waits behind the other's barriers. S_s(j) needs K(j) and its S columns free
-      // (separate P: the softmax read S_s(j-1), s_free; P aliasing S: PV_s(j-1) issued before it in
-      // the in-order tensor pipe). PV_s(j) needs V(j) and P_s(j) (p_full). A K / V unit is released
-      // once every head has issued the MMAs that read it.
-      int js[2] = {0, 0}, jp[2] = {0, nq > 1 ? 0 : n_kv};
-      if (nq == 1) js[1] = n_kv;
-      int kfree = 0, vfree = 0;
-      while (jp[0] < n_kv || jp[1] < n_kv) {
+      for (int k = 0; k < BN / 16; ++k)
+        umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
+      umma_commit(&bars->pv_done[s]);
+    };
+    mbar_wait(&bars->q_full, 0);
+    tc_fence_after();
+    // Event-driven issue: K/V units arrive in ring order K0 V0 K1 V1 ...; each head s has a next S
+    // tile js[s] and a next PV tile jp[s]; whatever is ready is issued (non-blocking probes, lane 0's
+    // answer broadcast so the warp stays converged), so one head never waits behind the other's
+    // barriers. S_s(j) needs K(j) and its S columns free (separate P: the softmax read S_s(j-1),
+    // s_free; P aliasing S: PV_s(j-1) issued before it in the in-order tensor pipe). PV_s(j) needs
+    // V(j) and P_s(j) (p_full). A K / V unit is released once every head has issued its MMAs.
+    int js[2] = {0, 0}, jp[2] = {0, nq > 1 ? 0 : n_kv};
+    if (nq == 1) js[1] = n_kv;
+    int kfree = 0, vfree = 0;
+    while (jp[0] < n_kv || jp[1] < n_kv) {
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const int j = js[s];
-          if (j < n_kv) {
-            const int itk = 2 * j, uk = itk % C::kUnits;
-            bool ok = mbar_test(&bars->kv_full[uk], (itk / C::kUnits) & 1);
-            if (ok && j > 0) ok = C::kPAlias ? jp[s] >= j : mbar_test(&bars->s_free[s], (j - 1) & 1);
-            if (ok) {
-              tc_fence_after();
-              issue_s(s, sKV + uk * C::kKVBytes);
-              js[s] = j + 1;
-            }
-          }
-          const int jv = jp[s];
-          if (jv < js[s]) {
-            const int itv = 2 * jv + 1, uv = itv % C::kUnits;
-            if (mbar_test(&bars->kv_full[uv], (itv / C::kUnits) & 1) && mbar_test(&bars->p_full[s], jv & 1)) {
-              tc_fence_after();
-              issue_pv(s, sKV + uv * C::kKVBytes, jv > 0);
-              jp[s] = jv + 1;
-            }
+      for (int s = 0; s < 2; ++s) {
+        const int j = js[s];
+        if (j < n_kv) {
+          const int itk = 2 * j, uk = itk % C::kUnits;
+          bool ok = mbar_test(&bars->kv_full[uk], (itk / C::kUnits) & 1);
+          if (ok && j > 0) ok = C::kPAlias ? jp[s] >= j : mbar_test(&bars->s_free[s], (j - 1) & 1);
+          if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
+            tc_fence_after();
+            if (elect_one()) issue_s(s, uk);
+            __syncwarp();
+            js[s] = j + 1;
           }
         }
-        for (; kfree < min(js[0], js[1]); ++kfree) umma_commit(&bars->kv_empty[(2 * kfree) % C::kUnits]);
-        for (; vfree < min(jp[0], jp[1]); ++vfree) umma_commit(&bars->kv_empty[(2 * vfree + 1) % C::kUnits]);
+        const int jv = jp[s];
+        if (jv < js[s]) {
+          const int itv = 2 * jv + 1, uv = itv % C::kUnits;
+          const bool ok = mbar_test(&bars->kv_full[uv], (itv / C::kUnits) & 1) && mbar_test(&bars->p_full[s], jv & 1);
+          if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
+            tc_fence_after();
+            if (elect_one()) issue_pv(s, uv, jv > 0);
+            __syncwarp();
+            jp[s] = jv + 1;
+          }
+        }
+      }
+      const int kf = min(js[0], js[1]), vf = min(jp[0], jp[1]);
+      if (kf > kfree || vf > vfree) {
+        if (elect_one()) {
+          for (int x = kfree; x < kf; ++x) umma_commit(&bars->kv_empty[(2 * x) % C::kUnits]);
+          for (int x = vfree; x < vf; ++x) umma_commit(&bars->kv_empty[(2 * x + 1) % C::kUnits]);
+        }
+        __syncwarp();
+        kfree = kf, vfree = vf;
       }
     }
   } else {

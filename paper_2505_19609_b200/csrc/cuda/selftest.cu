@@ -9,7 +9,8 @@ namespace skr {
 // smem: A 32 KB (two 64-wide chunks of 128 rows), B 32 KB, barriers.
 __global__ void __launch_bounds__(128, 1)
     selftest_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                    const __nv_bfloat16* __restrict__ A, float* __restrict__ C, int variant, int n) {
+                    const __nv_bfloat16* __restrict__ A, float* __restrict__ C, int variant, int n, int reps,
+                    long long* cycles, int chains) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -24,7 +25,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_init(bar_mma, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
   // variant 3: A [128][128] written by threads into SW128 K-major smem (as P is in attention)
   if (variant == 3) {
     const int row = threadIdx.x;
@@ -54,41 +55,63 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
   }
 
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // warp-converged issue loop; one elected lane issues (operands stay warp-uniform)
     const bool a_tma = variant != 3 && variant != 4;
     const bool b_mn = variant == 1 || variant == 2;
     const bool a_mn = variant == 2;
-    uint32_t bytes = (a_tma ? 32768u : 0u) + (b_mn ? (uint32_t)n * 256u : (uint32_t)n * 256u);
-    mbar_expect_tx(bar_tma, bytes);
-    for (int ch = 0; ch < 2; ++ch) {
-      if (a_tma) tma_load_2d(sA + ch * 16384, &ta, bar_tma, ch * 64, 0);  // 64 cols x 128 rows
+    uint32_t bytes = (a_tma ? 32768u : 0u) + (uint32_t)n * 256u;
+    if (elect_one()) {
+      mbar_expect_tx(bar_tma, bytes);
+      for (int ch = 0; ch < 2; ++ch) {
+        if (a_tma) tma_load_2d(sA + ch * 16384, &ta, bar_tma, ch * 64, 0);  // 64 cols x 128 rows
+      }
+      if (b_mn) {
+        // B global [K=128][n]: chunks of 64 n-columns x 128 K-rows
+        for (int ch = 0; ch < n / 64; ++ch) tma_load_2d(sB + ch * 16384, &tb, bar_tma, ch * 64, 0);
+      } else {
+        // B global [n][K=128]: chunks of 64 K-columns x n rows
+        for (int ch = 0; ch < 2; ++ch) tma_load_2d(sB + ch * (n * 128), &tb, bar_tma, ch * 64, 0);
+      }
     }
-    if (b_mn) {
-      // B global [K=128][n]: chunks of 64 n-columns x 128 K-rows
-      for (int ch = 0; ch < n / 64; ++ch) tma_load_2d(sB + ch * 16384, &tb, bar_tma, ch * 64, 0);
-    } else {
-      // B global [n][K=128]: chunks of 64 K-columns x n rows
-      for (int ch = 0; ch < 2; ++ch) tma_load_2d(sB + ch * (n * 128), &tb, bar_tma, ch * 64, 0);
-    }
+    __syncwarp();
     mbar_wait(bar_tma, 0);
     tc_fence_after();
     const uint32_t idesc = idesc_bf16_f32(128, n, a_mn ? 1 : 0, b_mn ? 1 : 0);
+    const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
+    uint64_t ad[8], bd[8];
+#pragma unroll
     for (int k = 0; k < 8; ++k) {
-      uint64_t ad, bd;
-      if (a_mn)
-        ad = sdesc_sw128(smem_u32(sA) + k * 2048, 16384, 1024);
-      else
-        ad = sdesc_sw128(smem_u32(sA) + (k / 4) * 16384 + (k % 4) * 32, 16, 1024);
-      if (b_mn)
-        bd = sdesc_sw128(smem_u32(sB) + k * 2048, 16384, 1024);
-      else
-        bd = sdesc_sw128(smem_u32(sB) + (k / 4) * (n * 128) + (k % 4) * 32, 16, 1024);
-      if (variant == 4)
-        umma_f16_ts(tmem, tmem + 128 + k * 8, bd, idesc, k > 0);
-      else
-        umma_f16(tmem, ad, bd, idesc, k > 0);
+      ad[k] = a_mn ? sdesc_sw128(sa + k * 2048, 16384, 1024) : sdesc_sw128(sa + (k / 4) * 16384 + (k % 4) * 32, 16, 1024);
+      bd[k] = b_mn ? sdesc_sw128(sb + k * 2048, 16384, 1024)
+                   : sdesc_sw128(sb + (k / 4) * (n * 128) + (k % 4) * 32, 16, 1024);
     }
-    umma_commit(bar_mma);
+    const long long t0 = clock64();
+    // one elected lane issues the whole MMA stream (descriptors precomputed, warp-uniform)
+    if (elect_one()) {
+      if (variant == 4) {
+        for (int rep = 0; rep < reps; ++rep)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t dcol = chains > 1 ? (uint32_t)((k % chains) * n) : 0u;
+            umma_f16_ts(tmem + dcol, tmem + 128 + k * 8, bd[k], idesc, chains > 1 ? (k >= chains) : (k > 0));
+          }
+      } else {
+        for (int rep = 0; rep < reps; ++rep)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t dcol = chains > 1 ? (uint32_t)((k % chains) * n) : 0u;
+            umma_f16(tmem + dcol, ad[k], bd[k], idesc, chains > 1 ? (k >= chains) : (k > 0));
+          }
+      }
+    }
+    __syncwarp();
+    if (elect_one()) umma_commit(bar_mma);
+    __syncwarp();
+    if (cycles) {
+      mbar_wait(bar_mma, 0);
+      if (lane == 0) cycles[0] = clock64() - t0;
+    }
   }
   __syncwarp();
   mbar_wait(bar_mma, 0);
@@ -102,7 +125,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<256>(tmem);
+  if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 }  // namespace skr
@@ -126,6 +149,26 @@ SKR_EXPORT skr_status skr_selftest_umma(int32_t variant, int32_t n, const void* 
   }
   const int smem = 65536 + 64 + 1024;
   cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  selftest_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(ta, tb, (const __nv_bfloat16*)A, C, variant, n);
+  selftest_kernel<<<1, 128, smem, (cudaStream_t)stream>>>(ta, tb, (const __nv_bfloat16*)A, C, variant, n, 1,
+                                                           nullptr, 1);
   return launch_status("selftest_kernel");
+}
+
+// Debug aid: cycles for `reps` x 8 UMMAs (128 x n x 16 each) of operand layout `variant` on one SM.
+extern "C" __attribute__((visibility("default"))) int skr_debug_umma_cycles(int variant, int n, int reps,
+                                                                           const void* A, const void* B,
+                                                                           float* C, long long* cycles,
+                                                                           int chains) {
+  using namespace skr;
+  CUtensorMap ta, tb;
+  const bool b_mn = variant == 1 || variant == 2;
+  make_tmap_2d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 128, 128, 128, 128, 64, true);
+  if (b_mn)
+    make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 128, n, n, 128, 64, true);
+  else
+    make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, 128, 128, n, 64, true);
+  const int smem = 65536 + 64 + 1024;
+  cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  selftest_kernel<<<1, 128, smem>>>(ta, tb, (const __nv_bfloat16*)A, C, variant, n, reps, cycles, chains);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
 }

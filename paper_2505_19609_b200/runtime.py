@@ -41,6 +41,7 @@ class RankStep:
         nd, ns = pr["n_dist_seg"], pr["n_seg"]
         cu, qp, ks, kl = pr["cu_seqlens_q"], pr["q_pos"], pr["k_start"], pr["k_len"]
         self.has_dist = self.nat_rows > 0
+        self.events = None          # list -> (kind, start, end) CUDA events around attention calls
         self.src_row = torch.as_tensor(pr["src_row"]).to(device)
         # segment classes: distributed chunks [0, nd), locals [nd, ns)
         self.dist_f = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "fwd", device)
@@ -97,17 +98,30 @@ class RankStep:
         sk.skr_gather_chunks(self.k_gath, self.chunks, self.n_chunks, self.k_nat, stream)
         sk.skr_gather_chunks(self.v_gath, self.chunks, self.n_chunks, self.v_nat, stream)
 
+    def _timed(self, kind, fn, stream):
+        if self.events is None:
+            return fn()
+        s = stream if stream is not None else torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fn()
+        e1.record(s)
+        self.events.append((kind, e0, e1))
+
     def fwd_local(self, stream=None):
-        sk.skr_attn_fwd(self.shape, self.loc_f, self.q, self.k, self.v, self.o, self.lse, stream)
+        self._timed("fwd", lambda: sk.skr_attn_fwd(self.shape, self.loc_f, self.q, self.k, self.v, self.o, self.lse,
+                                                   stream), stream)
 
     def fwd_dist(self, stream=None):
-        sk.skr_attn_fwd(self.shape, self.dist_f, self.q, self.k_nat, self.v_nat, self.o, self.lse, stream)
+        self._timed("fwd", lambda: sk.skr_attn_fwd(self.shape, self.dist_f, self.q, self.k_nat, self.v_nat, self.o,
+                                                   self.lse, stream), stream)
 
     def bwd_dist(self, stream=None):
         self.dk_nat.zero_()
         self.dv_nat.zero_()
-        sk.skr_attn_bwd(self.shape, self.dist_b, self.q, self.k_nat, self.v_nat, self.o, self.do, self.lse, self.dq,
-                        self.dk_nat, self.dv_nat, 1, self.ws, stream)
+        self._timed("bwd", lambda: sk.skr_attn_bwd(self.shape, self.dist_b, self.q, self.k_nat, self.v_nat, self.o,
+                                                   self.do, self.lse, self.dq, self.dk_nat, self.dv_nat, 1, self.ws,
+                                                   stream), stream)
 
     def grad_scatter(self, stream=None):
         sk.skr_scatter_chunks(self.dk_nat, self.chunks, self.n_chunks, self.P, self.cp, self.dk_rm, stream)
@@ -124,8 +138,8 @@ class RankStep:
                 sk.skr_cast_f32_bf16(self.dv_red[:n], self.dv[:n], stream)
 
     def bwd_local(self, stream=None):
-        sk.skr_attn_bwd(self.shape, self.loc_b, self.q, self.k, self.v, self.o, self.do, self.lse, self.dq, self.dk,
-                        self.dv, 0, self.ws, stream)
+        self._timed("bwd", lambda: sk.skr_attn_bwd(self.shape, self.loc_b, self.q, self.k, self.v, self.o, self.do,
+                                                   self.lse, self.dq, self.dk, self.dv, 0, self.ws, stream), stream)
 
     # ------------------------------------------------------------------ production composition
     def forward(self, q_src, k_src, v_src, comm=None, side=None):
