@@ -104,7 +104,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -151,8 +151,7 @@ def ncu_traffic(workload, world, kind):
         with open(p) as f:
             j = json.load(f)
         e = j[f"{workload}/n{world}"][f"attn_{kind}"]
-        return {"bytes_per_launch": e["dram_bytes"], "launches_per_step": e.get("launches_per_step"),
-                "source": e.get("source", "profiles/ncu_summary.json")}
+        return float(e["dram_bytes"]), e.get("source", "profiles/ncu_summary.json")
     except Exception:
         return None
 
@@ -370,7 +369,9 @@ def run_ours(args):
                        "rollbacks": int(plan["n_rollbacks"]),
                        "l2": "inputs larger than L2 (no flush)", "parallelism": f"cp{cp}"},
             "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]}", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic[0] if traffic else None,
+                         "traffic_source": traffic[1] if traffic else None,
                          "peak_source": f"{which} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
             "cpu_baseline": cpu,
             "e2e": None if e2e is None else {"value": total_flops / (float(allv[:, 3].max()) * 1e-3) / 1e12,

@@ -29,6 +29,7 @@ namespace bwd {
 
 // Debug timeline (SKR_TRACE=1): (event, clock) pairs of block (0, 0) into a device buffer.
 __device__ unsigned long long* g_trace = nullptr;
+__device__ int g_skip_math = 0;   // debug: compute / dQ warpgroups only signal (pipeline timing)
 __device__ unsigned int g_trace_n = 0;
 __device__ __forceinline__ void trace(int ev) {
   if (g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
@@ -254,10 +255,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
       const bool more = n + 1 < n_steps;
       mbar_wait(&bars->s_free, n & 1);
-      trace(1);
+      if (lane == 0) trace(1);
       if (more) {
         mbar_wait(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
-        trace(2);
+        if (lane == 0) trace(2);
         tc_fence_after();
         if (elect_one()) {
           issue_t(dK, dQ + st1 * qstage, C::tS);
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       mbar_wait(&bars->p_full, n & 1);
-      trace(3);
+      if (lane == 0) trace(3);
       tc_fence_after();
       if (elect_one()) {
         issue_kv(false, dDOmn + st * qstage, C::tDV, n > 0);
@@ -285,12 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mbar_wait(&bars->ds_full, n & 1);
-      trace(4);
+      if (lane == 0) trace(4);
       tc_fence_after();
       if (elect_one()) issue_kv(true, dQmn + st * qstage, C::tDK, n > 0);
       __syncwarp();
       mbar_wait(&bars->dq_empty, (n & 1) ^ 1);
-      trace(5);
+      if (lane == 0) trace(5);
       tc_fence_after();
       if (elect_one()) {
         issue_dq();
@@ -324,6 +325,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->s_full, n & 1);
       if (threadIdx.x == 0) trace(10);
       tc_fence_after();
+      if (g_skip_math) {
+        tc_fence_before();
+        mbar_arrive(&bars->s_free);
+        if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);
+        mbar_arrive(&bars->p_full);
+        mbar_wait(&bars->dp_full, n & 1);
+        mbar_arrive(&bars->dp_free);
+        if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);
+        mbar_arrive(&bars->ds_full);
+        if (threadIdx.x == 0) trace(13);
+        continue;
+      }
       float p[H];
 #pragma unroll
       for (int c = 0; c < H; c += 32) {
@@ -447,6 +460,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->dq_full, n & 1);
       if (t == 0) trace(20);
       tc_fence_after();
+      if (g_skip_math) {
+        mbar_arrive(&bars->dq_empty);
+        continue;
+      }
       // the previous step's reduce must have finished reading the smem tile
       if (warp == 8 && elect_one()) bulk_wait_read<0>();
       named_bar_sync(1, 128);
@@ -555,6 +572,8 @@ static unsigned long long* trace_buffer() {
     if (getenv("SKR_TRACE")) {
       cudaMalloc(&buf, 8192 * sizeof(unsigned long long));
       cudaMemcpyToSymbol(bwd::g_trace, &buf, sizeof(buf));
+      const int skip = getenv("SKR_SKIP_MATH") ? 1 : 0;
+      cudaMemcpyToSymbol(bwd::g_skip_math, &skip, sizeof(skip));
     }
   }
   return buf;

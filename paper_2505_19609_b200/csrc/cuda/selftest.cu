@@ -87,6 +87,26 @@ __global__ void __launch_bounds__(128, 1)
                    : sdesc_sw128(sb + (k / 4) * (n * 128) + (k % 4) * 32, 16, 1024);
     }
     const long long t0 = clock64();
+    if (chains < 0) {
+      // latency mode: groups of -chains MMAs, each followed by commit + wait (serialised groups)
+      const int g = -chains;
+      uint32_t ph = 1;   // bar_mma phase 0 is used by the final commit below; start at phase 1 parity
+      uint64_t* bar2 = bar_mma + 2;
+      if (elect_one()) mbar_init(bar2, 1);
+      __syncwarp();
+      fence_mbar_init();
+      ph = 0;
+      for (int rep = 0; rep < reps; ++rep) {
+        if (elect_one()) {
+          for (int k = 0; k < g; ++k) umma_f16(tmem, ad[k & 7], bd[k & 7], idesc, k > 0);
+          umma_commit(bar2);
+        }
+        __syncwarp();
+        mbar_wait(bar2, ph);
+        ph ^= 1;
+        tc_fence_after();
+      }
+    } else
     // one elected lane issues the whole MMA stream (descriptors precomputed, warp-uniform)
     if (elect_one()) {
       if (variant == 4) {
