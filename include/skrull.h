@@ -109,6 +109,13 @@ skr_status skr_gds(const int64_t* lens, int32_t K, const skr_cluster* cl, const 
 skr_status skr_plan(const int64_t* lens, int32_t K, const skr_cluster* cl, const skr_model* m, int32_t* dp_of_seq,
                     int32_t* mb_of_seq, int32_t* assign, int32_t* n_mb_per_dp, int32_t* n_rollbacks);
 
+/* Baselines (row f1): Alg. 4 round-robin (R27: input order, shard by N, R6 roll-back on
+ * RemainBucket) -> assign[K] as skr_dacp; and the DeepSpeed-like full-shard plan (S:398-406, P:101,
+ * P:316): FIFO micro-batches under C*N tokens (mb_of_seq[K], n_mb), every sequence distributed. */
+skr_status skr_round_robin(const int64_t* lens, int32_t K, const skr_cluster* cl, int32_t* assign,
+                           int32_t* n_rollbacks, int32_t* fail_idx);
+skr_status skr_full_shard(const int64_t* lens, int32_t K, const skr_cluster* cl, int32_t* mb_of_seq, int32_t* n_mb);
+
 /* ------------------------------------------------------------------ a4: packer (host)
  * One micro-batch (mb_lens[K_mb] in micro-batch input order, its DACP assign), CP rank `rank`.
  * Layout (R20-R23): zigzag chunks c of 2N, [floor(cS/2N), floor((c+1)S/2N)), rank j owns j and

@@ -291,3 +291,77 @@ SKR_EXPORT skr_status skr_plan(const int64_t* lens, int32_t K, const skr_cluster
   if (n_rollbacks) *n_rollbacks = nrb;
   return SKR_OK;
 }
+
+// ---------------------------------------------------------------------------- baselines (row f1)
+// Alg. 4 round-robin (reading R27: all K sequences in input order, shard by N), with the
+// R6 roll-back on the RemainBucket ledger only (RR keeps no load array), and the DeepSpeed-like
+// full-shard plan: FIFO micro-batches under C*N tokens, all distributed.
+SKR_EXPORT skr_status skr_round_robin(const int64_t* lens, int32_t K, const skr_cluster* cl, int32_t* assign,
+                                      int32_t* n_rollbacks, int32_t* fail_idx) {
+  SKR_REQUIRE(cl && K >= 0 && (K == 0 || (lens && assign)) && cl->cp >= 1, "skr_round_robin: bad arguments");
+  const int32_t N = cl->cp;
+  std::vector<i128> RB(N, (i128)N * cl->bucket_tokens);   // scaled by N (R4)
+  std::vector<int32_t> ret(K, kUnassigned);
+  int32_t nrb = 0;
+  int32_t i = 0;
+  while (i < K) {
+    SKR_REQUIRE(lens[i] >= 0, "skr_round_robin: negative length");
+    int32_t t = 0;                                        // FindMaxBucketsIds (lowest on ties)
+    for (int32_t j = 1; j < N; ++j)
+      if (RB[j] > RB[t]) t = j;
+    if (RB[t] >= (i128)N * lens[i]) {
+      ret[i] = t, RB[t] -= (i128)N * lens[i], ++i;
+      continue;
+    }
+    int32_t m = 0;                                        // FindMinBucketsIds
+    for (int32_t j = 1; j < N; ++j)
+      if (RB[j] < RB[m]) m = j;
+    if (RB[m] >= (i128)lens[i]) {                          // C[j] >= S[i]/N
+      ret[i] = -1;
+      for (int32_t j = 0; j < N; ++j) RB[j] -= lens[i];
+      ++i;
+      continue;
+    }
+    int32_t v = -1;
+    if (cl->rollback)
+      for (int32_t q = 0; q < K; ++q)
+        if (ret[q] == m) {
+          v = q;
+          break;
+        }
+    if (v < 0) {
+      if (fail_idx) *fail_idx = i;
+      if (n_rollbacks) *n_rollbacks = nrb;
+      return fail(SKR_E_SCHEDULE, "round-robin: sequence %d cannot be placed (%s)", i,
+                  cl->rollback ? "roll-back impossible" : "roll-back disabled");
+    }
+    ret[v] = -1;
+    RB[m] += (i128)N * lens[v];
+    for (int32_t j = 0; j < N; ++j) RB[j] -= lens[v];
+    ++nrb;
+  }
+  for (int32_t k = 0; k < K; ++k) assign[k] = ret[k];
+  if (n_rollbacks) *n_rollbacks = nrb;
+  if (fail_idx) *fail_idx = -1;
+  return SKR_OK;
+}
+
+SKR_EXPORT skr_status skr_full_shard(const int64_t* lens, int32_t K, const skr_cluster* cl, int32_t* mb_of_seq,
+                                     int32_t* n_mb) {
+  SKR_REQUIRE(cl && n_mb && K >= 0 && (K == 0 || (lens && mb_of_seq)) && cl->cp >= 1,
+              "skr_full_shard: bad arguments");
+  const i128 cap = (i128)cl->bucket_tokens * cl->cp;
+  int32_t mb = 0;
+  i128 tot = 0;
+  bool open = false;
+  for (int32_t k = 0; k < K; ++k) {
+    if (lens[k] > (i128)cl->bucket_tokens * cl->cp)
+      return fail(SKR_E_SCHEDULE, "full-shard: sequence %d (%lld tokens) exceeds C*N", k, (long long)lens[k]);
+    if (open && tot + lens[k] > cap) ++mb, tot = 0;
+    mb_of_seq[k] = mb;
+    tot += lens[k];
+    open = true;
+  }
+  *n_mb = open ? mb + 1 : 0;
+  return SKR_OK;
+}

@@ -234,6 +234,30 @@ def skr_plan(lens, bucket, cp, dp, hidden, kv_hidden, pack_batch=1, rollback=Tru
     return dict(dp_of_seq=dpo, mb_of_seq=mbo, assign=asg, n_mb_per_dp=nmb, n_rollbacks=nrb.value)
 
 
+def skr_round_robin(lens, bucket, cp, rollback=True):
+    """Alg. 4 baseline -> (assign int32[K], n_rollbacks)."""
+    L = np.ascontiguousarray(lens, np.int64)
+    A = np.zeros(len(L), np.int32)
+    nrb, fidx = i32(), i32()
+    st = _sig("skr_round_robin", i32, P(i64), i32, P(skr_cluster), P(i32), P(i32), P(i32))(
+        _ptr(L, i64), len(L), C.byref(_cluster(cp, 1, bucket, rollback)), _ptr(A, i32), C.byref(nrb), C.byref(fidx))
+    if st != SKR_OK:
+        e = SkrullError(st, _lib.skr_last_error().decode())
+        e.fail_idx = fidx.value
+        raise e
+    return A, nrb.value
+
+
+def skr_full_shard(lens, bucket, cp):
+    """Full-shard baseline -> (mb_of_seq int32[K], n_mb); every sequence is distributed."""
+    L = np.ascontiguousarray(lens, np.int64)
+    M = np.zeros(len(L), np.int32)
+    n = i32()
+    _check(_sig("skr_full_shard", i32, P(i64), i32, P(skr_cluster), P(i32), P(i32))(
+        _ptr(L, i64), len(L), C.byref(_cluster(cp, 1, bucket)), _ptr(M, i32), C.byref(n)))
+    return M, n.value
+
+
 # ---------------------------------------------------------------------------- a4 packer
 def skr_pack_bounds(mb_lens, assign, cp, rank):
     L = np.ascontiguousarray(mb_lens, np.int64)

@@ -182,3 +182,37 @@ def test_tiles_cover_work_once_and_are_lpt_ordered():
         tb = skrull.skr_tiles_bwd(cu, qp, kl, n, 128)
         assert sorted(map(tuple, tb)) == sorted((s, t) for s in range(n) if ql[s] > 0
                                                 for t in range(-(-kl[s] // 128)))
+
+
+def test_baselines_bit_exact_fuzz():
+    # row f1: Alg. 4 round-robin and full-shard vs the oracle
+    from oracle.schedule import full_shard, round_robin
+    rng = random.Random(16)
+    for _ in range(800):
+        N = rng.choice([1, 2, 4, 8])
+        K = rng.randint(0, 50)
+        L = _lens(rng, K)
+        C = rng.randint(1, max(2, sum(L) // N + 1000))
+        rb = rng.random() < 0.8
+        try:
+            ref = round_robin(L, C, N, rb)
+        except ScheduleError as e:
+            with pytest.raises(skrull.SkrullError) as ce:
+                skrull.skr_round_robin(L, C, N, rb)
+            assert ce.value.fail_idx == e.pos
+            continue
+        A, _ = skrull.skr_round_robin(L, C, N, rb)
+        assert list(A) == ref
+        try:
+            mbs = full_shard(L, C, N)
+        except ScheduleError:
+            with pytest.raises(skrull.SkrullError):
+                skrull.skr_full_shard(L, C, N)
+            continue
+        M, n = skrull.skr_full_shard(L, C, N)
+        assert n == len(mbs)
+        assert all(M[k] == j for j, mb in enumerate(mbs) for k in mb)
+    # Table 3 structure: both heuristics fail without roll-back on [50,60,90], C=100, N=2
+    with pytest.raises(skrull.SkrullError):
+        skrull.skr_round_robin([50, 60, 90], 100, 2, rollback=False)
+    assert list(skrull.skr_round_robin([50, 60, 90], 100, 2)[0]).count(-1) >= 1

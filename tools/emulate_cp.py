@@ -1,0 +1,103 @@
+#!/usr/bin/env python
+"""Row f1 measurement: DACP vs the paper's baseline plans on the attention path, one GPU.
+
+    python tools/emulate_cp.py --config C5n8 [--schedulers skrull,dacp-only,rr,full-shard]
+
+An N-rank CP group is emulated on ONE B200: every rank's packed micro-batch is run through the same
+C-ABI kernels as production (RankStep phases; the all-gather / reduce-scatter replaced by device
+copies), and each rank's attention fwd + bwd kernel time is measured with CUDA events. The
+emulated step time is the Eq. 8-style sum over micro-batches of the slowest rank (Eq. 1
+P:154); communication is not included (NVLink is not available on one GPU). Schedulers:
+  skrull     : GDS micro-batching (Alg. 2) + DACP (Alg. 1/3)
+  dacp-only  : FIFO micro-batches under C*N tokens + DACP (the step-by-step ablation)
+  rr         : FIFO micro-batches + round-robin placement (Alg. 4)
+  full-shard : FIFO micro-batches, every sequence sharded (DeepSpeed-like baseline)
+Prints one JSON line per scheduler.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def plans(sk, name, lens, C, N, h, hkv):
+    """-> list of (mb_lens, mb_assign) for one global batch under scheduler `name`."""
+    if name == "skrull":
+        p = sk.skr_plan(lens, C, N, 1, h, hkv)
+        out = []
+        for j in range(int(p["n_mb_per_dp"][0])):
+            idx = np.nonzero(p["mb_of_seq"] == j)[0]
+            out.append((lens[idx], p["assign"][idx]))
+        return out
+    mbo, n = sk.skr_full_shard(lens, C, N)
+    out = []
+    for j in range(n):
+        idx = np.nonzero(mbo == j)[0]
+        ml = lens[idx]
+        if name == "full-shard":
+            a = np.full(len(ml), -1, np.int32)
+        elif name == "dacp-only":
+            a, _ = sk.skr_dacp(ml, C, N, h, hkv)
+        elif name == "rr":
+            a, _ = sk.skr_round_robin(ml, C, N)
+        else:
+            raise ValueError(name)
+        out.append((ml, a))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C5n8")
+    ap.add_argument("--schedulers", default="skrull,dacp-only,rr,full-shard")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+    from paper_2505_19609_b200 import skrull as sk
+    from paper_2505_19609_b200.runtime import RankStep, loopback_step
+    from synth import CONFIGS
+    cfg = CONFIGS[a.config]
+    lens = cfg.lengths(a.seed)
+    N, C, shp = cfg.cp, cfg.bucket, cfg.shape
+    shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
+    useful = sum(14 * shp.d * shp.hq * int(S) * (int(S) + 1) // 2 for S in lens)
+    g = torch.Generator(device="cuda").manual_seed(a.seed)
+    for name in a.schedulers.split(","):
+        mbs = plans(sk, name, lens, C, N, shp.hidden, shp.kv_hidden)
+        step_ms, per_rank_tot, n_dist = 0.0, np.zeros(N), 0
+        for ml, ma in mbs:
+            n_dist += int((ma == -1).sum())
+            ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
+            srcs = {k: [torch.randn(max(rs.rows, 1), shp.hq if k in ("q", "do") else shp.hkv, shp.d, device="cuda",
+                                    generator=g).bfloat16() for rs in ranks] for k in ("q", "k", "v", "do")}
+            loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])      # warm-up
+            best = np.full(N, np.inf)
+            for _ in range(a.reps):
+                for rs in ranks:
+                    rs.events = []
+                loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+                torch.cuda.synchronize()
+                t = np.array([sum(e0.elapsed_time(e1) for _, e0, e1 in rs.events) for rs in ranks])
+                best = np.minimum(best, t)
+            for rs in ranks:
+                rs.events = None
+            step_ms += best.max()
+            per_rank_tot += best
+            del ranks, srcs
+            torch.cuda.empty_cache()
+        out = {"scheduler": name, "config": a.config, "cp": N, "bucket": C, "micro_batches": len(mbs),
+               "distributed_seqs": n_dist, "emulated_step_ms": step_ms,
+               "useful_tflops_per_gpu": useful / (step_ms * 1e-3) / N / 1e12,
+               "max_over_mean_rank_time": float(per_rank_tot.max() / per_rank_tot.mean()),
+               "note": "attention kernels only, one GPU, N ranks emulated; comm excluded"}
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
