@@ -106,6 +106,31 @@ __global__ void __launch_bounds__(128, 1)
         ph ^= 1;
         tc_fence_after();
       }
+    } else if (chains >= 100) {
+      // mixed-stream mode (chains = 100 + m): m = 0 SS/TS alternating into one accumulator,
+      // m = 1 SS N=n / SS N=64 alternating idesc into two accumulators, m = 2 SS into 2 accumulators,
+      // m = 3 TS/SS alternating into two accumulators
+      const int m = chains - 100;
+      const uint32_t id64 = idesc_bf16_f32(128, 64, a_mn ? 1 : 0, b_mn ? 1 : 0);
+      if (elect_one()) {
+        for (int rep = 0; rep < reps; ++rep)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (m == 0) {
+              if (k & 1) umma_f16_ts(tmem, tmem + 128 + k * 8, bd[k], idesc, 1);
+              else umma_f16(tmem, ad[k], bd[k], idesc, k > 0);
+            } else if (m == 1) {
+              if (k & 1) umma_f16(tmem + 256, ad[k], bd[k], id64, k > 1);
+              else umma_f16(tmem, ad[k], bd[k], idesc, k > 0);
+            } else if (m == 2) {
+              umma_f16(tmem + (k & 1) * 256, ad[k], bd[k], idesc, k > 1);
+            } else {
+              if (k & 1) umma_f16_ts(tmem + 256, tmem + 128 + k * 8, bd[k], idesc, k > 1);
+              else umma_f16(tmem, ad[k], bd[k], idesc, k > 0);
+            }
+          }
+      }
+      __syncwarp();
     } else
     // one elected lane issues the whole MMA stream (descriptors precomputed, warp-uniform)
     if (elect_one()) {

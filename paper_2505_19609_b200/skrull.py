@@ -435,7 +435,11 @@ class Comm:
             _check(_sig("skr_nccl_get_id", i32, vp)(C.cast(buf, vp)))
         t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
         if nranks > 1:
+            # an NCCL process group only moves device tensors; gloo takes host tensors
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
             dist.broadcast(t, src=0, group=group)
+            t = t.cpu()
         buf = (C.c_uint8 * n)(*t.tolist())
         self.h = vp()
         _check(_sig("skr_comm_create", i32, vp, i32, i32, P(vp))(C.cast(buf, vp), int(nranks), int(rank),
