@@ -348,13 +348,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars->s_free);                   // S TMEM may be overwritten by S(n+1)
+      const float2 sl2_2 = make_float2(sl2, sl2);
 #pragma unroll
       for (int i = 0; i < H; i += 4) {
-        const float4 l4 = ld_shared_f4(a_lse + i * 4);
-        p[i + 0] = ex2(fmaf(p[i + 0], sl2, -l4.x));
-        p[i + 1] = ex2(fmaf(p[i + 1], sl2, -l4.y));
-        p[i + 2] = ex2(fmaf(p[i + 2], sl2, -l4.z));
-        p[i + 3] = ex2(fmaf(p[i + 3], sl2, -l4.w));
+        const float4 l4 = ld_shared_f4(a_lse + i * 4);     // -lse2 is folded: p * sl2 - lse2
+        const float2 e0 = ffma2(make_float2(p[i], p[i + 1]), sl2_2, make_float2(-l4.x, -l4.y));
+        const float2 e1 = ffma2(make_float2(p[i + 2], p[i + 3]), sl2_2, make_float2(-l4.z, -l4.w));
+        p[i + 0] = ex2(e0.x);
+        p[i + 1] = ex2(e0.y);
+        p[i + 2] = ex2(e1.x);
+        p[i + 3] = ex2(e1.y);
       }
       if (diag) {
 #pragma unroll
@@ -388,10 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
-          p[c + i + 0] *= __uint_as_float(r[i + 0]) - d4.x;
-          p[c + i + 1] *= __uint_as_float(r[i + 1]) - d4.y;
-          p[c + i + 2] *= __uint_as_float(r[i + 2]) - d4.z;
-          p[c + i + 3] *= __uint_as_float(r[i + 3]) - d4.w;
+          const float2 t0 = fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(-d4.x, -d4.y));
+          const float2 t1 = fadd2(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])),
+                                  make_float2(-d4.z, -d4.w));
+          const float2 s0 = fmul2(make_float2(p[c + i], p[c + i + 1]), t0);
+          const float2 s1 = fmul2(make_float2(p[c + i + 2], p[c + i + 3]), t1);
+          p[c + i + 0] = s0.x, p[c + i + 1] = s0.y, p[c + i + 2] = s1.x, p[c + i + 3] = s1.y;
         }
       }
       if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem / TMEM free

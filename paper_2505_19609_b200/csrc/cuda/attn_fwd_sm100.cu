@@ -254,21 +254,25 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         // P = exp2(S * scale * log2e - m_ref) into registers (bf16 pairs) before waiting for PV(j-1),
         // so the PV MMA has the whole exponential phase to complete.
         const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};               // 4 independent row-sum chains
+        // packed fp32x2 FFMA / FADD: two elements per instruction; 2 x float2 = 4 row-sum chains
+        float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
         uint32_t pk[BN / 2];
 #pragma unroll
         for (int c = 0; c < BN; c += 8) {
           float pv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float xx = fmaf(x[c + i], sl2, neg_m);
+          for (int i = 0; i < 8; i += 2) {
+            const float2 xx = ffma2(make_float2(x[c + i], x[c + i + 1]), sl2_2, nm2);
             // some exponentials on the FMA pipe, the rest on MUFU (MUFU ex2 is the d=64 bound)
-            pv[i] = (i % 8) < kPolyPer8 ? ex2_poly(xx) : ex2(xx);
-            ls[i % 4] += pv[i];
+            pv[i] = i < kPolyPer8 ? ex2_poly(xx.x) : ex2(xx.x);
+            pv[i + 1] = i + 1 < kPolyPer8 ? ex2_poly(xx.y) : ex2(xx.y);
+            ls2[(i / 2) % 2] = fadd2(ls2[(i / 2) % 2], make_float2(pv[i], pv[i + 1]));
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
         }
+        const float ls[4] = {ls2[0].x, ls2[0].y, ls2[1].x, ls2[1].y};
         // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
         if (j > 0) {
           mbar_wait(&bars->pv_done[s], (j - 1) & 1);
@@ -281,7 +285,11 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
             tmem_ld16(tO + c, r);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            for (int i = 0; i < 16; i += 2) {
+              const float2 v = fmul2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                     make_float2(alpha, alpha));
+              r[i] = __float_as_uint(v.x), r[i + 1] = __float_as_uint(v.y);
+            }
             tmem_st16(tO + c, r);
           }
         }

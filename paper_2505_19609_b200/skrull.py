@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libskrull.so")
+# SKR_LIB_PATH: load another in-tree build of the same library (A/B performance experiments)
+LIB_PATH = os.environ.get("SKR_LIB_PATH") or os.path.join(_HERE, "libskrull.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2505_19609_b200.build`")
