@@ -42,7 +42,8 @@ def _flags():
     inc = ["-I", INCLUDE, "-I", CSRC]
     if nccl:
         inc += ["-I", os.path.join(nccl, "include")]
-    cu = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+    trace = ["-DSKR_KERNEL_TRACE"] if os.environ.get("SKR_KERNEL_TRACE") else []   # debug timelines only
+    cu = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", *trace,
           "--expt-relaxed-constexpr", "-Xptxas", "-v", *inc]
     cc = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
           "-Wno-unused-parameter", "-I", os.path.join(CUDA, "include"), *inc]

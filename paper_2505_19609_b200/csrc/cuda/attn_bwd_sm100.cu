@@ -30,12 +30,27 @@ namespace bwd {
 // Debug timeline (SKR_TRACE=1): (event, clock) pairs of block (0, 0) into a device buffer.
 __device__ unsigned long long* g_trace = nullptr;
 __device__ int g_skip_math = 0;   // debug: compute / dQ warpgroups only signal (pipeline timing)
-__device__ unsigned int g_trace_n = 0;
+#ifdef SKR_KERNEL_TRACE
+constexpr bool kSkipMath = true;
+#else
+constexpr bool kSkipMath = false;
+#endif
+// fire-and-forget store (no atomics: a returning atomic would cost ~1000 cycles on the traced path);
+// each recording thread owns a 2048-entry slice chosen by its role
+__shared__ int g_trace_cnt[8];
+__device__ __forceinline__ void trace_init() {
+#ifdef SKR_KERNEL_TRACE
+  if (threadIdx.x < 8) g_trace_cnt[threadIdx.x] = 0;
+#endif
+}
 __device__ __forceinline__ void trace(int ev) {
+#ifdef SKR_KERNEL_TRACE   // debug builds only: production kernels carry no instrumentation
   if (g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
-    const unsigned int i = atomicAdd(&g_trace_n, 1u);
-    if (i < 8192) g_trace[i] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+    const int role = ev / 10 < 8 ? ev / 10 : 7;
+    const int i = g_trace_cnt[role]++;
+    g_trace[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
   }
+#endif
 }
 
 constexpr int BN = 128;  // key tile
@@ -134,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->dp_free, kComputeThreads);
     fence_mbar_init();
   }
+  trace_init();
   if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->s_full, n & 1);
       if (threadIdx.x == 0) trace(10);
       tc_fence_after();
-      if (g_skip_math) {
+      if (kSkipMath && g_skip_math) {
         tc_fence_before();
         mbar_arrive(&bars->s_free);
         if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);
@@ -465,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->dq_full, n & 1);
       if (t == 0) trace(20);
       tc_fence_after();
-      if (g_skip_math) {
+      if (kSkipMath && g_skip_math) {
         mbar_arrive(&bars->dq_empty);
         continue;
       }
@@ -576,6 +592,7 @@ static unsigned long long* trace_buffer() {
     init = true;
     if (getenv("SKR_TRACE")) {
       cudaMalloc(&buf, 8192 * sizeof(unsigned long long));
+      cudaMemset(buf, 0, 8192 * sizeof(unsigned long long));
       cudaMemcpyToSymbol(bwd::g_trace, &buf, sizeof(buf));
       const int skip = getenv("SKR_SKIP_MATH") ? 1 : 0;
       cudaMemcpyToSymbol(bwd::g_skip_math, &skip, sizeof(skip));
@@ -588,14 +605,10 @@ static unsigned long long* trace_buffer() {
 extern "C" __attribute__((visibility("default"))) int skr_debug_bwd_trace(unsigned long long* out, int cap) {
   unsigned long long* buf = trace_buffer();
   if (!buf) return 0;
-  unsigned int n = 0;
-  cudaMemcpyFromSymbol(&n, bwd::g_trace_n, sizeof(n));
-  n = n > 8192 ? 8192 : n;
-  n = (int)n > cap ? cap : n;
+  const int n = cap < 8192 ? cap : 8192;
   cudaMemcpy(out, buf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  unsigned int z = 0;
-  cudaMemcpyToSymbol(bwd::g_trace_n, &z, sizeof(z));
-  return (int)n;
+  cudaMemset(buf, 0, 8192 * sizeof(unsigned long long));
+  return n;
 }
 
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,

@@ -25,6 +25,26 @@
 namespace skr {
 namespace fwd {
 
+// Debug timeline (SKR_TRACE=1): (event, clock) pairs of block (0, 0) into a device buffer.
+__device__ unsigned long long* g_trace = nullptr;
+// fire-and-forget store (no atomics: a returning atomic would cost ~1000 cycles on the traced path);
+// each recording thread owns a 2048-entry slice chosen by its role
+__shared__ int g_trace_cnt[8];
+__device__ __forceinline__ void trace_init() {
+#ifdef SKR_KERNEL_TRACE
+  if (threadIdx.x < 8) g_trace_cnt[threadIdx.x] = 0;
+#endif
+}
+__device__ __forceinline__ void trace(int ev) {
+#ifdef SKR_KERNEL_TRACE   // debug builds only: production kernels carry no instrumentation
+  if (g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
+    const int role = ev / 10 < 8 ? ev / 10 : 7;
+    const int i = g_trace_cnt[role]++;
+    g_trace[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+  }
+#endif
+}
+
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -93,6 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
     }
     fence_mbar_init();
   }
+  trace_init();
   if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -118,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
       for (int kv = 0; kv < 2; ++kv, ++it) {
         const int u = it % C::kUnits;
         mbar_wait(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+        if (lane == 0) trace(40 + kv);
         if (elect_one()) {
           mbar_expect_tx(&bars->kv_full[u], C::kKVBytes);
           uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
@@ -172,11 +194,15 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         if (j < n_kv) {
           const int itk = 2 * j, uk = itk % C::kUnits;
           bool ok = mbar_test(&bars->kv_full[uk], (itk / C::kUnits) & 1);
+          const bool kready = ok;
           if (ok && j > 0) ok = C::kPAlias ? jp[s] >= j : mbar_test(&bars->s_free[s], (j - 1) & 1);
+          if (lane == 0 && !ok && kready) trace(9);   // K resident, waiting for the softmax to free S
           if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
             tc_fence_after();
+            if (lane == 0) trace(5 + s);
             if (elect_one()) issue_s(s, uk);
             __syncwarp();
+            if (lane == 0) trace(1 + s);
             js[s] = j + 1;
           }
         }
@@ -186,8 +212,10 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           const bool ok = mbar_test(&bars->kv_full[uv], (itv / C::kUnits) & 1) && mbar_test(&bars->p_full[s], jv & 1);
           if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
             tc_fence_after();
+            if (lane == 0) trace(7 + s);
             if (elect_one()) issue_pv(s, uv, jv > 0);
             __syncwarp();
+            if (lane == 0) trace(3 + s);
             jp[s] = jv + 1;
           }
         }
@@ -217,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&bars->s_full[s], j & 1);
+        if (row == 0) trace(10 + 10 * s);
         tc_fence_after();
         float x[BN];
 #pragma unroll
@@ -273,11 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
         }
         const float ls[4] = {ls2[0].x, ls2[0].y, ls2[1].x, ls2[1].y};
+        if (row == 0) trace(11 + 10 * s);
         // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
         if (j > 0) {
           mbar_wait(&bars->pv_done[s], (j - 1) & 1);
           tc_fence_after();
         }
+        if (row == 0) trace(12 + 10 * s);
         if (rescale && j > 0) {
 #pragma unroll
           for (int c = 0; c < D; c += 16) {
@@ -304,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
+        if (row == 0) trace(13 + 10 * s);
       }
       // ---- epilogue: O / l -> bf16, LSE
       mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
@@ -338,8 +370,33 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
 
 }  // namespace fwd
 
+static unsigned long long* fwd_trace_buffer() {
+  static unsigned long long* buf = nullptr;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    if (getenv("SKR_TRACE")) {
+      cudaMalloc(&buf, 8192 * sizeof(unsigned long long));
+      cudaMemset(buf, 0, 8192 * sizeof(unsigned long long));
+      cudaMemcpyToSymbol(fwd::g_trace, &buf, sizeof(buf));
+    }
+  }
+  return buf;
+}
+
+// Debug aid: copy the last fwd trace (event << 48 | clock) to host; returns the number of entries.
+extern "C" __attribute__((visibility("default"))) int skr_debug_fwd_trace(unsigned long long* out, int cap) {
+  unsigned long long* buf = fwd_trace_buffer();
+  if (!buf) return 0;
+  const int n = cap < 8192 ? cap : 8192;
+  cudaMemcpy(out, buf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemset(buf, 0, 8192 * sizeof(unsigned long long));
+  return n;
+}
+
 skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k, const void* v, void* o, float* lse,
                           int n_q_rows, int n_kv_rows, cudaStream_t st) {
+  fwd_trace_buffer();
   if (a.n_tiles == 0) return SKR_OK;
   CUtensorMap tq, tk, tv;
   const uint64_t qcols = (uint64_t)a.hq * d, kcols = (uint64_t)a.hkv * d;

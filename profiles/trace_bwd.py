@@ -22,7 +22,7 @@ for _ in range(2):
     sk.skr_attn_bwd(shape, bs, q, k, v, o, do, lse, dq, dk, dv, 0, ws)
     torch.cuda.synchronize()
 n = sk._lib.skr_debug_bwd_trace(buf, 8192)
-ev = np.array([(x >> 48, x & ((1 << 48) - 1)) for x in buf[:n]])
+ev = np.array([(x >> 48, x & ((1 << 48) - 1)) for x in buf[:n] if x])
 ev = ev[np.argsort(ev[:, 1], kind="stable")]
 t0 = ev[0, 1]
 names = {1: "M s_free", 2: "M qdo", 3: "M p_full", 4: "M ds_full", 5: "M dq_empty", 10: "C s_full", 11: "C p_arrive",
