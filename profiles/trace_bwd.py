@@ -1,4 +1,7 @@
-"""Debug timeline of one backward CTA (SKR_TRACE=1): prints per-step event times in cycles."""
+"""Debug timeline of one backward CTA (SKR_TRACE=1): prints per-step event times in cycles.
+
+Needs an instrumented library: SKR_KERNEL_TRACE=1 python -m paper_2505_19609_b200.build --clean
+(production builds compile the trace hooks out; rebuild without the variable afterwards)."""
 import ctypes, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
