@@ -18,8 +18,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build")
-LIB = os.path.join(PKG, "libskrull.so")
+# SKR_KERNEL_TRACE=1: instrumented debug build into its own objects / library (load it with
+# SKR_LIB_PATH=.../libskrull_trace.so); the production library never carries the trace hooks
+_TRACE = bool(os.environ.get("SKR_KERNEL_TRACE"))   # "1": event timeline, "phase": phase accounting
+BUILD = os.path.join(ROOT, "build_trace" if _TRACE else "build")
+LIB = os.path.join(PKG, "libskrull_trace.so" if _TRACE else "libskrull.so")
 INCLUDE = os.path.join(ROOT, "include")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
@@ -42,7 +45,11 @@ def _flags():
     inc = ["-I", INCLUDE, "-I", CSRC]
     if nccl:
         inc += ["-I", os.path.join(nccl, "include")]
-    trace = ["-DSKR_KERNEL_TRACE"] if os.environ.get("SKR_KERNEL_TRACE") else []   # debug timelines only
+    trace = []   # debug timelines only
+    if _TRACE:
+        trace.append("-DSKR_PHASE_ACCT" if os.environ["SKR_KERNEL_TRACE"] == "phase" else "-DSKR_KERNEL_TRACE")
+    if _TRACE and os.environ.get("SKR_TRACE_SOFTMAX"):
+        trace.append("-DSKR_TRACE_SOFTMAX")
     cu = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", *trace,
           "--expt-relaxed-constexpr", "-Xptxas", "-v", *inc]
     cc = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",

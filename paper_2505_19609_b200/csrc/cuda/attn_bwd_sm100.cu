@@ -38,17 +38,20 @@ constexpr bool kSkipMath = false;
 // fire-and-forget store (no atomics: a returning atomic would cost ~1000 cycles on the traced path);
 // each recording thread owns a 2048-entry slice chosen by its role
 __shared__ int g_trace_cnt[8];
+__shared__ unsigned long long* g_trace_smem;   // this block's buffer (null: not traced), read from smem
 __device__ __forceinline__ void trace_init() {
 #ifdef SKR_KERNEL_TRACE
   if (threadIdx.x < 8) g_trace_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) g_trace_smem = (blockIdx.x == 0 && blockIdx.y == 0) ? g_trace : nullptr;
 #endif
 }
 __device__ __forceinline__ void trace(int ev) {
 #ifdef SKR_KERNEL_TRACE   // debug builds only: production kernels carry no instrumentation
-  if (g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
+  unsigned long long* buf = g_trace_smem;
+  if (buf != nullptr) {
     const int role = ev / 10 < 8 ? ev / 10 : 7;
     const int i = g_trace_cnt[role]++;
-    g_trace[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+    buf[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
   }
 #endif
 }

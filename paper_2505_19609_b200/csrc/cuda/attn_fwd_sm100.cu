@@ -30,20 +30,75 @@ __device__ unsigned long long* g_trace = nullptr;
 // fire-and-forget store (no atomics: a returning atomic would cost ~1000 cycles on the traced path);
 // each recording thread owns a 2048-entry slice chosen by its role
 __shared__ int g_trace_cnt[8];
+__shared__ unsigned long long* g_trace_smem;   // this block's buffer (null: not traced), read from smem
 __device__ __forceinline__ void trace_init() {
-#ifdef SKR_KERNEL_TRACE
+#if defined(SKR_KERNEL_TRACE) || defined(SKR_PHASE_ACCT)
   if (threadIdx.x < 8) g_trace_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) g_trace_smem = (blockIdx.x == 0 && blockIdx.y == 0) ? g_trace : nullptr;
 #endif
 }
-__device__ __forceinline__ void trace(int ev) {
+__device__ __forceinline__ void trace(int ev, int j = 0) {   // j: tile index payload (8 bits)
 #ifdef SKR_KERNEL_TRACE   // debug builds only: production kernels carry no instrumentation
-  if (g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
+  unsigned long long* buf = g_trace_smem;
+  if (buf != nullptr) {
     const int role = ev / 10 < 8 ? ev / 10 : 7;
     const int i = g_trace_cnt[role]++;
-    g_trace[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+    buf[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | ((unsigned long long)(j & 0xFF) << 40) |
+                                     (clock64() & 0xFFFFFFFFFFull);
   }
 #endif
 }
+// per-warp event (several warps share the role slice: shared atomic slot), debug builds only
+__device__ __forceinline__ void trace_w(int ev, int j) {
+#ifdef SKR_KERNEL_TRACE
+  unsigned long long* buf = g_trace_smem;
+  if (buf != nullptr) {
+    const int role = ev / 10 < 8 ? ev / 10 : 7;
+    const int i = atomicAdd(&g_trace_cnt[role], 1);
+    buf[role * 1024 + (i & 1023)] = ((unsigned long long)ev << 48) | ((unsigned long long)(j & 0xFF) << 40) |
+                                     (clock64() & 0xFFFFFFFFFFull);
+  }
+#endif
+}
+
+// softmax-side events perturb the warpgroup they are recorded from (the traced warp falls behind
+// its siblings and every 128-arrival barrier waits for it): separate opt-in, SKR_TRACE_SOFTMAX
+#ifdef SKR_TRACE_SOFTMAX
+__device__ __forceinline__ void trace_sm(int ev, int j) { trace(ev, j); }
+__device__ __forceinline__ void trace_smw(int ev, int j) { trace_w(ev, j); }
+#else
+__device__ __forceinline__ void trace_sm(int, int) {}
+__device__ __forceinline__ void trace_smw(int, int) {}
+#endif
+
+// Phase accounting (SKR_PHASE_ACCT builds): per-warp cycle totals of each phase of the loop kept in
+// registers and written once at the end (block (0, 0) only) - no events on the path, so the
+// warps are not perturbed the way per-event traces perturb them.
+struct PhaseAcct {
+#ifdef SKR_PHASE_ACCT
+  long long t, acc[8];
+  __device__ __forceinline__ void start() {
+    t = clock64();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0;
+  }
+  __device__ __forceinline__ void mark(int k) {
+    const long long n = clock64();
+    acc[k] += n - t;
+    t = n;
+  }
+  __device__ __forceinline__ void flush(int slot) {
+    unsigned long long* b = g_trace_smem;
+    if (b != nullptr)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[slot * 8 + k] = (unsigned long long)acc[k];
+  }
+#else
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush(int) {}
+#endif
+};
 
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 320;
@@ -134,12 +189,16 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
       }
     }
     __syncwarp();
+    PhaseAcct pa;   // 0 waiting for a free unit, 1 issuing
+    pa.start();
     int it = 0;
     for (int j = 0; j < n_kv; ++j) {
       for (int kv = 0; kv < 2; ++kv, ++it) {
         const int u = it % C::kUnits;
-        mbar_wait(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
-        if (lane == 0) trace(40 + kv);
+        pa.mark(1);
+        mbar_wait_sleep(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+        pa.mark(0);
+        if (lane == 0) trace(40 + kv, j);
         if (elect_one()) {
           mbar_expect_tx(&bars->kv_full[u], C::kKVBytes);
           uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
@@ -150,86 +209,117 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         __syncwarp();
       }
     }
+    pa.mark(1);
+    if (lane == 0) pa.flush(8);
   } else if (warp == 9) {
-    // ================= MMA issuer: the warp runs the control flow converged (descriptors stay
-    // warp-uniform, no per-instruction ELECT/R2UR waterfall); one elected lane issues each MMA group.
-    const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0);   // S = Q K^T   (both K-major)
-    const uint32_t id_o = idesc_bf16_f32(BM, D, 0, 1);    // O += P V    (V is MN-major)
-    const uint32_t sQ = smem_u32(smem + C::kOffQ), sKV = smem_u32(smem + C::kOffKV);
-    // descriptor of (base + off) == descriptor of base + (off >> 4): the start address is the low field
-    const uint64_t dq0 = sdesc_sw128(sQ, 16, 1024), dkv0 = sdesc_sw128(sKV, 16, 1024);
-    const uint64_t dv0 = sdesc_sw128(sKV, BN * 128, 1024);
-    auto issue_s = [&](int s, int u) {
-      const uint64_t dq = dq0 + ((uint32_t)(s * C::kQBytes) >> 4), dk = dkv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
+    // ================= MMA issuer: ONE elected thread runs the whole loop. Measured (profiles/
+    // umma_probe.py): the tensor pipe buffers only about one MMA ahead of the issuing thread, and
+    // re-entering an elected region per MMA group costs ~200 cycles (R2UR of the descriptors,
+    // BSSY/ELECT); inside a single elect.sync region groups + commits stream at the MMA floor.
+    if (elect_one()) {
+      const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0);   // S = Q K^T   (both K-major)
+      const uint32_t id_o = idesc_bf16_f32(BM, D, 0, 1);    // O += P V    (V is MN-major)
+      const uint32_t sQ = smem_u32(smem + C::kOffQ), sKV = smem_u32(smem + C::kOffKV);
+      // descriptor of (base + off) == descriptor of base + (off >> 4): the start address is the low field
+      const uint64_t dq0 = sdesc_sw128(sQ, 16, 1024), dkv0 = sdesc_sw128(sKV, 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(sKV, BN * 128, 1024);
+      auto issue_s = [&](int s, int u) {
+        const uint64_t dq = dq0 + ((uint32_t)(s * C::kQBytes) >> 4), dk = dkv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
 #pragma unroll
-      for (int k = 0; k < D / 16; ++k) {
-        const uint32_t off = ((k / 4) * (BM * 128) + (k % 4) * 32) >> 4;
-        const uint32_t koff = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
-        umma_f16(tmem + C::tS(s), dq + off, dk + koff, id_s, k > 0);
-      }
-      umma_commit(&bars->s_full[s]);
-    };
-    auto issue_pv = [&](int s, int u, bool acc) {
-      const uint64_t dv = dv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = ((k / 4) * (BM * 128) + (k % 4) * 32) >> 4;
+          const uint32_t koff = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
+          umma_f16(tmem + C::tS(s), dq + off, dk + koff, id_s, k > 0);
+        }
+        umma_commit(&bars->s_full[s]);
+      };
+      auto issue_pv = [&](int s, int u, bool acc) {
+        const uint64_t dv = dv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
 #pragma unroll
-      for (int k = 0; k < BN / 16; ++k)
-        umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
-      umma_commit(&bars->pv_done[s]);
-    };
-    mbar_wait(&bars->q_full, 0);
-    tc_fence_after();
-    // Event-driven issue: K/V units arrive in ring order K0 V0 K1 V1 ...; each head s has a next S
-    // tile js[s] and a next PV tile jp[s]; whatever is ready is issued (non-blocking probes, lane 0's
-    // answer broadcast so the warp stays converged), so one head never waits behind the other's
-    // barriers. S_s(j) needs K(j) and its S columns free (separate P: the softmax read S_s(j-1),
-    // s_free; P aliasing S: PV_s(j-1) issued before it in the in-order tensor pipe). PV_s(j) needs
-    // V(j) and P_s(j) (p_full). A K / V unit is released once every head has issued its MMAs.
-    int js[2] = {0, 0}, jp[2] = {0, nq > 1 ? 0 : n_kv};
-    if (nq == 1) js[1] = n_kv;
-    int kfree = 0, vfree = 0;
-    while (jp[0] < n_kv || jp[1] < n_kv) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int j = js[s];
-        if (j < n_kv) {
-          const int itk = 2 * j, uk = itk % C::kUnits;
-          bool ok = mbar_test(&bars->kv_full[uk], (itk / C::kUnits) & 1);
-          const bool kready = ok;
-          if (ok && j > 0) ok = C::kPAlias ? jp[s] >= j : mbar_test(&bars->s_free[s], (j - 1) & 1);
-          if (lane == 0 && !ok && kready) trace(9);   // K resident, waiting for the softmax to free S
-          if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
-            tc_fence_after();
-            if (lane == 0) trace(5 + s);
-            if (elect_one()) issue_s(s, uk);
-            __syncwarp();
-            if (lane == 0) trace(1 + s);
-            js[s] = j + 1;
+        for (int k = 0; k < BN / 16; ++k)
+          umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
+        umma_commit(&bars->pv_done[s]);
+      };
+      mbar_wait_sleep(&bars->q_full, 0);
+      tc_fence_after();
+      // Static schedule with blocking waits (K/V units arrive in ring order K0 V0 K1 V1 ...). An
+      // event-driven loop that polls every barrier was measured slower: with the tensor pipe only
+      // ~one MMA ahead of the issuing thread, every poll between groups is pipe idle time.
+      //  separate P (d=64):  [S_A(j) S_B(j)] release K(j); [PV_A(j-1) PV_B(j-1)] release V(j-1).
+      //    S_s(j) waits until the softmax has read S_s(j-1) (s_free), so it overlaps softmax(j-1).
+      //  P aliasing S (d=128): per head [PV_s(j-1) S_s(j)] back to back: S_s(j) overwrites P_s(j-1)
+      //    after the in-order pipe has consumed it, and never queues behind the other head's PV.
+      auto kunit = [&](int j) { return (2 * j) % C::kUnits; };
+      auto vunit = [&](int j) { return (2 * j + 1) % C::kUnits; };
+      PhaseAcct pa;   // 0 waiting for K, 1 for V, 2 for S free / P full, 3 issuing
+      pa.start();
+      auto wait_k = [&](int j) {
+        pa.mark(3);
+        mbar_wait_sleep(&bars->kv_full[kunit(j)], ((2 * j) / C::kUnits) & 1);
+        pa.mark(0);
+      };
+      auto wait_v = [&](int j) {
+        pa.mark(3);
+        mbar_wait_sleep(&bars->kv_full[vunit(j)], ((2 * j + 1) / C::kUnits) & 1);
+        pa.mark(1);
+      };
+      if (!C::kPAlias) {
+        for (int j = 0; j <= n_kv; ++j) {
+          if (j < n_kv) {
+            wait_k(j);
+            for (int s = 0; s < nq; ++s) {
+              pa.mark(3);
+              if (j > 0) mbar_wait_sleep(&bars->s_free[s], (j - 1) & 1);
+              pa.mark(2);
+              tc_fence_after();
+              trace(5 + s, j);
+              issue_s(s, kunit(j));
+              trace(1 + s, j);
+            }
+            umma_commit(&bars->kv_empty[kunit(j)]);   // K(j) free once every head's S MMAs completed
+          }
+          if (j > 0) {
+            const int jv = j - 1;
+            wait_v(jv);
+            for (int s = 0; s < nq; ++s) {
+              pa.mark(3);
+              mbar_wait_sleep(&bars->p_full[s], jv & 1);
+              pa.mark(2);
+              tc_fence_after();
+              trace(7 + s, jv);
+              issue_pv(s, vunit(jv), jv > 0);
+              trace(3 + s, jv);
+            }
+            umma_commit(&bars->kv_empty[vunit(jv)]);
           }
         }
-        const int jv = jp[s];
-        if (jv < js[s]) {
-          const int itv = 2 * jv + 1, uv = itv % C::kUnits;
-          const bool ok = mbar_test(&bars->kv_full[uv], (itv / C::kUnits) & 1) && mbar_test(&bars->p_full[s], jv & 1);
-          if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
+      } else {
+        wait_k(0);
+        tc_fence_after();
+        for (int s = 0; s < nq; ++s) issue_s(s, kunit(0));
+        umma_commit(&bars->kv_empty[kunit(0)]);
+        for (int j = 1; j <= n_kv; ++j) {
+          const int jv = j - 1;
+          wait_v(jv);
+          if (j < n_kv) wait_k(j);
+          for (int s = 0; s < nq; ++s) {
+            pa.mark(3);
+            mbar_wait_sleep(&bars->p_full[s], jv & 1);
+            pa.mark(2);
             tc_fence_after();
-            if (lane == 0) trace(7 + s);
-            if (elect_one()) issue_pv(s, uv, jv > 0);
-            __syncwarp();
-            if (lane == 0) trace(3 + s);
-            jp[s] = jv + 1;
+            trace(7 + s, jv);
+            issue_pv(s, vunit(jv), jv > 0);
+            if (j < n_kv) issue_s(s, kunit(j));
+            trace(3 + s, jv);
           }
+          umma_commit(&bars->kv_empty[vunit(jv)]);
+          if (j < n_kv) umma_commit(&bars->kv_empty[kunit(j)]);
         }
       }
-      const int kf = min(js[0], js[1]), vf = min(jp[0], jp[1]);
-      if (kf > kfree || vf > vfree) {
-        if (elect_one()) {
-          for (int x = kfree; x < kf; ++x) umma_commit(&bars->kv_empty[(2 * x) % C::kUnits]);
-          for (int x = vfree; x < vf; ++x) umma_commit(&bars->kv_empty[(2 * x + 1) % C::kUnits]);
-        }
-        __syncwarp();
-        kfree = kf, vfree = vf;
-      }
+      pa.mark(3);
+      pa.flush(9);
     }
+    __syncwarp();
   } else {
     // ================= softmax warpgroups
     const int s = warp / 4;                 // 0 -> head A, 1 -> head B
@@ -243,22 +333,33 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
       const int qp = qp0 + row;                // this row's query position
       const float sl2 = a.scale * 1.4426950408889634f;
       float m_ref = -INFINITY, l = 0.f;
+      // (a strict ping-pong of the two heads' exp phases through named barriers was measured slower:
+      // one warp alone drives the MUFU at ~70% of its rate, two overlapping warps at ~92%)
+      PhaseAcct pa;   // 0 wait S, 1 TMEM load S, 2 mask + max, 3 wait PV, 4 rescale + store P, 6 exps
+      pa.start();
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&bars->s_full[s], j & 1);
-        if (row == 0) trace(10 + 10 * s);
+        pa.mark(0);
+        if (lane == 0) trace_smw(30 + 20 * s + 0, j | (warp % 4) << 6);
         tc_fence_after();
+        // all four 32-column loads in flight under one wait (a wait per load serialises ~4 TMEM
+        // round trips on the path to s_free and the exponentials)
         float x[BN];
+        {
+          uint32_t r[BN / 32][32];
 #pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tS + c, r);
+          for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + 32 * c, r[c]);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[c + i] = __uint_as_float(r[i]);
+          for (int c = 0; c < BN / 32; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[32 * c + i] = __uint_as_float(r[c][i]);
         }
         if (!C::kPAlias) {
           tc_fence_before();
           mbar_arrive(&bars->s_free[s]);      // S_s TMEM may now take S_s(j+1)
+          pa.mark(1);
+          if (lane == 0) trace_smw(30 + 20 * s + 1, j | (warp % 4) << 6);
         }
         const int kv0 = j * BN;
         if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
@@ -266,15 +367,18 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           for (int i = 0; i < BN; ++i)
             if (kv0 + i > qp) x[i] = -INFINITY;
         }
-        // row max with 8 independent chains (a single 128-long fmax chain is ~512 cycles of latency)
+        // row max: 8 independent chains of three-input max (a single 128-long chain is latency-bound)
         float mxs[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mxs[i] = x[i];
 #pragma unroll
-        for (int i = 8; i < BN; ++i) mxs[i % 8] = fmaxf(mxs[i % 8], x[i]);
+        for (int i = 8; i < BN; i += 16)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mxs[t] = fmax3(mxs[t], x[i + t], i + 8 + t < BN ? x[i + 8 + t] : x[i + t]);
         const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
                                fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
         const float m_new = fmaxf(m_ref, mx * sl2);
+        pa.mark(2);
         // tcgen05.ld/st are warp-collective: the rescale decision is made per warp (every lane of
         // the warp moves its reference max to its own m_new; alpha == 1 where nothing changed)
         const bool rescale = __any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0;
@@ -283,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         // P = exp2(S * scale * log2e - m_ref) into registers (bf16 pairs) before waiting for PV(j-1),
         // so the PV MMA has the whole exponential phase to complete.
         const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+        pa.mark(2);
         // packed fp32x2 FFMA / FADD: two elements per instruction; 2 x float2 = 4 row-sum chains
         float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
@@ -302,13 +407,15 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
         }
         const float ls[4] = {ls2[0].x, ls2[0].y, ls2[1].x, ls2[1].y};
-        if (row == 0) trace(11 + 10 * s);
+        if (lane == 0) trace_smw(30 + 20 * s + 2, j | (warp % 4) << 6);
+        pa.mark(6);
         // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
         if (j > 0) {
           mbar_wait(&bars->pv_done[s], (j - 1) & 1);
           tc_fence_after();
         }
-        if (row == 0) trace(12 + 10 * s);
+        pa.mark(3);
+        if (lane == 0) trace_smw(30 + 20 * s + 3, j | (warp % 4) << 6);
         if (rescale && j > 0) {
 #pragma unroll
           for (int c = 0; c < D; c += 16) {
@@ -335,8 +442,10 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
-        if (row == 0) trace(13 + 10 * s);
+        pa.mark(4);
+        if (lane == 0) trace_smw(30 + 20 * s + 4, j | (warp % 4) << 6);
       }
+      if (lane == 0) pa.flush(warp);
       // ---- epilogue: O / l -> bf16, LSE
       mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
       tc_fence_after();
@@ -413,7 +522,9 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
     const int v = e ? atoi(e) : -1;
     return (v >= 0 && v <= 3) ? v : -1;
   }();
-  const int pp = poly >= 0 ? poly : (d == 64 ? 1 : 0);   // measured: more poly only adds issue pressure
+  // measured (profiles/fwd_period.py, S = 32K): d=64 best at 2/8, d=128 at 1/8; beyond that the
+  // polynomial's FMA / ALU instructions cost more issue slots than the MUFU time they save
+  const int pp = poly >= 0 ? poly : (d == 64 ? 2 : 1);
   auto launch = [&](auto kern, int smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);

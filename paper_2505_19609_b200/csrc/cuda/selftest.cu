@@ -106,6 +106,58 @@ __global__ void __launch_bounds__(128, 1)
         ph ^= 1;
         tc_fence_after();
       }
+    } else if (chains >= 200) {
+      // issue-path probe mode (chains = 200 + m): `reps` warp-converged groups of 4 MMAs, each group
+      // committed to bar2 (never waited), then m = 0 nothing, 1 mbarrier probe of an idle barrier,
+      // 2 probe of bar2 itself, 3 a plain shared-memory load, 4 probe of an idle barrier without
+      // the commit. Cycles of the whole sequence (does a barrier probe wait for the committed MMAs?)
+      const int m = (chains - 200) % 10;
+      const int gs = (chains - 200) / 10 == 1 ? 8 : (chains - 200) / 10 == 2 ? 2 : 4;   // MMAs per group
+      uint64_t* bar2 = bar_mma + 2;
+      uint64_t* bar3 = bar_mma + 3;
+      if (elect_one()) { mbar_init(bar2, 1); mbar_init(bar3, 1); }
+      __syncwarp();
+      fence_mbar_init();
+      int acc = 0;
+      volatile int* vs = reinterpret_cast<volatile int*>(bar_mma + 4);
+      if (m == 6) {
+        // control: the same groups + commits, all inside one elected region (no per-group election)
+        if (elect_one()) {
+          for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) umma_f16(tmem, ad[k], bd[k], idesc, k > 0 || rep > 0);
+            umma_commit(bar2);
+          }
+        }
+        __syncwarp();
+      }
+      for (int rep = 0; rep < (m == 6 ? 0 : reps); ++rep) {
+        if (elect_one()) {
+          if (m == 5) {
+            // descriptors formed inside the issue block from the shared-memory bases (uniform values)
+            const uint64_t a0 = sdesc_sw128(sa, 16, 1024), b0 = sdesc_sw128(sb, 16, 1024);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_f16(tmem, a0 + (uint64_t)(((k / 4) * 16384 + (k % 4) * 32) >> 4),
+                       b0 + (uint64_t)(((k / 4) * (n * 128) + (k % 4) * 32) >> 4), idesc, k > 0 || rep > 0);
+          } else if (gs == 2) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) umma_f16(tmem, ad[k], bd[k], idesc, k > 0 || rep > 0);
+          } else if (gs == 4) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) umma_f16(tmem, ad[k], bd[k], idesc, k > 0 || rep > 0);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) umma_f16(tmem, ad[k], bd[k], idesc, k > 0 || rep > 0);
+          }
+          if (m != 4) umma_commit(bar2);
+        }
+        __syncwarp();
+        if (m == 1 || m == 4) acc += __shfl_sync(0xffffffffu, mbar_test(bar3, 0) ? 1 : 0, 0);
+        else if (m == 2) acc += __shfl_sync(0xffffffffu, mbar_test(bar2, rep & 1) ? 1 : 0, 0);
+        else if (m == 3) acc += vs[lane];
+      }
+      if (lane == 0 && cycles) cycles[1] = acc;   // mode 2: how many probes found their own group complete
     } else if (chains >= 100) {
       // mixed-stream mode (chains = 100 + m): m = 0 SS/TS alternating into one accumulator,
       // m = 1 SS N=n / SS N=64 alternating idesc into two accumulators, m = 2 SS into 2 accumulators,
@@ -212,8 +264,50 @@ extern "C" __attribute__((visibility("default"))) int skr_debug_umma_cycles(int 
     make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 128, n, n, 128, 64, true);
   else
     make_tmap_2d(&tb, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, 128, 128, n, 64, true);
-  const int smem = 65536 + 64 + 1024;
+  const int smem = 65536 + 1024 + 1024;   // + barriers / probe words of the debug modes
   cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   selftest_kernel<<<1, 128, smem>>>(ta, tb, (const __nv_bfloat16*)A, C, variant, n, reps, cycles, chains);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
+
+// Debug aid: MUFU ex2 throughput. `warps` warps (one CTA, one SM) each run `iters` x 16 independent
+// ex2.approx (8 chains); mode 1 interleaves each ex2 with one FFMA2 + FADD2 + F2FP (the softmax mix).
+namespace skr {
+__global__ void mufu_kernel(int iters, int mode, long long* cycles, float* sink) {
+  float x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = 0.001f * (threadIdx.x + i);
+  uint32_t pk = 0;
+  float2 acc = make_float2(0.f, 0.f);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      if (mode == 1) {
+        const float2 xx = ffma2(make_float2(x[i], x[i + 1]), make_float2(0.5f, 0.5f), make_float2(-0.25f, -0.25f));
+        x[i] = ex2(xx.x);
+        x[i + 1] = ex2(xx.y);
+        acc = fadd2(acc, make_float2(x[i], x[i + 1]));
+        pk ^= pack_bf16(x[i], x[i + 1]);
+      } else {
+        x[i] = ex2(x[i] * -0.5f);
+        x[i + 1] = ex2(x[i + 1] * -0.5f);
+      }
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[0] = t1 - t0;
+  float s = acc.x + acc.y + (float)pk;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i];
+  if (s == 12345.f) sink[0] = s;
+}
+}  // namespace skr
+
+extern "C" __attribute__((visibility("default"))) int skr_debug_mufu_cycles(int warps, int iters, int mode,
+                                                                           long long* cycles, float* sink) {
+  skr::mufu_kernel<<<1, warps * 32>>>(iters, mode, cycles, sink);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
 }

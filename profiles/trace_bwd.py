@@ -1,11 +1,13 @@
 """Debug timeline of one backward CTA (SKR_TRACE=1): prints per-step event times in cycles.
 
-Needs an instrumented library: SKR_KERNEL_TRACE=1 python -m paper_2505_19609_b200.build --clean
-(production builds compile the trace hooks out; rebuild without the variable afterwards)."""
+Needs the instrumented library (production builds compile the trace hooks out):
+    SKR_KERNEL_TRACE=1 python -m paper_2505_19609_b200.build   # -> libskrull_trace.so (loaded below)"""
 import ctypes, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["SKR_TRACE"] = "1"
+os.environ.setdefault("SKR_LIB_PATH", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                   "paper_2505_19609_b200", "libskrull_trace.so"))
 import torch
 from paper_2505_19609_b200 import skrull as sk
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 64
