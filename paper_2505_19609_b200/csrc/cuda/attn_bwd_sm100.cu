@@ -30,17 +30,12 @@ namespace bwd {
 // Debug timeline (SKR_TRACE=1): (event, clock) pairs of block (0, 0) into a device buffer.
 __device__ unsigned long long* g_trace = nullptr;
 __device__ int g_skip_math = 0;   // debug: compute / dQ warpgroups only signal (pipeline timing)
-#ifdef SKR_KERNEL_TRACE
-constexpr bool kSkipMath = true;
-#else
-constexpr bool kSkipMath = false;
-#endif
 // fire-and-forget store (no atomics: a returning atomic would cost ~1000 cycles on the traced path);
 // each recording thread owns a 2048-entry slice chosen by its role
 __shared__ int g_trace_cnt[8];
 __shared__ unsigned long long* g_trace_smem;   // this block's buffer (null: not traced), read from smem
 __device__ __forceinline__ void trace_init() {
-#ifdef SKR_KERNEL_TRACE
+#if defined(SKR_KERNEL_TRACE) || defined(SKR_PHASE_ACCT)
   if (threadIdx.x < 8) g_trace_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) g_trace_smem = (blockIdx.x == 0 && blockIdx.y == 0) ? g_trace : nullptr;
 #endif
@@ -100,6 +95,7 @@ struct Bars {
   uint64_t qdo_full[3], qdo_empty[3];
   uint64_t s_full, dp_full, p_full, ds_full, dv_done, dsq_done, dq_full, dq_empty;
   uint64_t s_free, dp_free;
+  uint64_t mma_done;   // single phase: every MMA of the CTA has completed (dK / dV epilogue)
   uint32_t tmem_base;
 };
 
@@ -112,13 +108,15 @@ struct StepIter {
   }
 };
 
-template <int D>
+// kPolyPer8: how many of every 8 exponentials run as a polynomial on the FMA pipe (the exp phase of
+// the two compute warpgroups is MUFU-bound).
+template <int D, int kPolyPer8>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, AttnArgs a, const float* __restrict__ lse,
                     const float* __restrict__ Dbuf, void* __restrict__ dk_out, void* __restrict__ dv_out,
-                    int accumulate) {
+                    int accumulate, float* __restrict__ dq_acc) {
   using C = Cfg<D>;
   constexpr int BQ = C::BQ, H = C::H;
   extern __shared__ uint8_t smem_raw[];
@@ -150,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->dq_empty, 128);
     mbar_init(&bars->s_free, kComputeThreads);
     mbar_init(&bars->dp_free, kComputeThreads);
+    mbar_init(&bars->mma_done, 1);
     fence_mbar_init();
   }
   trace_init();
@@ -213,8 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (n + 1 < n_steps) fetch(it);
     }
   } else if (warp == 13) {
-    // ================= MMA issuer: warp-converged control flow, one elected lane issues each group
-    // (issuing from a divergent lane makes every tcgen05.mma an ELECT/R2UR waterfall, ~100 cycles).
+    // ================= MMA issuer (one elect.sync-elected thread; see below)
     const uint32_t sK = smem_u32(smem + C::kOffK), sV = smem_u32(smem + C::kOffV);
     const uint32_t sQ = smem_u32(smem + C::kOffQ), sDO = smem_u32(smem + C::kOffDO);
     const uint32_t sDS = smem_u32(smem + C::kOffDS);
@@ -257,62 +255,66 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     const uint32_t qstage = (uint32_t)C::kQBytes >> 4;
-    mbar_wait(&bars->kv_full, 0);
-    mbar_wait(&bars->qdo_full[0], 0);
-    tc_fence_after();
+    // ONE elected thread runs the whole issue loop: re-entering an elected region per MMA group costs
+    // ~200 cycles (descriptor R2UR + ELECT/BSSY) while the tensor pipe buffers only ~one MMA ahead of
+    // the issuing thread (profiles/umma_probe.py), so per-group election left the pipe idle.
     if (elect_one()) {
+      PhaseAcct pa;   // waits: 0 s_free, 1 qdo_full, 2 p_full, 3 dp_free, 4 ds_full, 5 dq_empty; 6 issue
+      pa.start();
+      mbar_wait_sleep(&bars->kv_full, 0);
+      mbar_wait_sleep(&bars->qdo_full[0], 0);
+      tc_fence_after();
       issue_t(dK, dQ, C::tS);
       umma_commit(&bars->s_full);
       issue_t(dV, dDO, C::tDP);
       umma_commit(&bars->dp_full);
-    }
-    __syncwarp();
-    // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its own
-    // columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows dK(n)
-    // in the in-order tensor pipe.
-    for (int n = 0; n < n_steps; ++n) {
-      const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
-      const bool more = n + 1 < n_steps;
-      mbar_wait(&bars->s_free, n & 1);
-      if (lane == 0) trace(1);
-      if (more) {
-        mbar_wait(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
-        if (lane == 0) trace(2);
-        tc_fence_after();
-        if (elect_one()) {
+      // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its
+      // own columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows
+      // dK(n) in the in-order tensor pipe.
+      for (int n = 0; n < n_steps; ++n) {
+        const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
+        const bool more = n + 1 < n_steps;
+        pa.mark(6);
+        mbar_wait_sleep(&bars->s_free, n & 1);
+        pa.mark(0);
+        trace(1);
+        if (more) {
+          pa.mark(6);
+          mbar_wait_sleep(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
+          pa.mark(1);
+          trace(2);
+          tc_fence_after();
           issue_t(dK, dQ + st1 * qstage, C::tS);
           umma_commit(&bars->s_full);
         }
-        __syncwarp();
-      }
-      mbar_wait(&bars->p_full, n & 1);
-      if (lane == 0) trace(3);
-      tc_fence_after();
-      if (elect_one()) {
+        pa.mark(6);
+        mbar_wait_sleep(&bars->p_full, n & 1);
+        pa.mark(2);
+        trace(3);
+        tc_fence_after();
         issue_kv(false, dDOmn + st * qstage, C::tDV, n > 0);
         umma_commit(&bars->dv_done);
-      }
-      __syncwarp();
-      if (!C::kDSAlias) {
-        mbar_wait(&bars->dp_free, n & 1);
-        if (more) {
-          tc_fence_after();
-          if (elect_one()) {
+        if (!C::kDSAlias) {
+          pa.mark(6);
+          mbar_wait_sleep(&bars->dp_free, n & 1);
+          pa.mark(3);
+          if (more) {
+            tc_fence_after();
             issue_t(dV, dDO + st1 * qstage, C::tDP);
             umma_commit(&bars->dp_full);
           }
-          __syncwarp();
         }
-      }
-      mbar_wait(&bars->ds_full, n & 1);
-      if (lane == 0) trace(4);
-      tc_fence_after();
-      if (elect_one()) issue_kv(true, dQmn + st * qstage, C::tDK, n > 0);
-      __syncwarp();
-      mbar_wait(&bars->dq_empty, (n & 1) ^ 1);
-      if (lane == 0) trace(5);
-      tc_fence_after();
-      if (elect_one()) {
+        pa.mark(6);
+        mbar_wait_sleep(&bars->ds_full, n & 1);
+        pa.mark(4);
+        trace(4);
+        tc_fence_after();
+        issue_kv(true, dQmn + st * qstage, C::tDK, n > 0);
+        pa.mark(6);
+        mbar_wait_sleep(&bars->dq_empty, (n & 1) ^ 1);
+        pa.mark(5);
+        trace(5);
+        tc_fence_after();
         issue_dq();
         umma_commit(&bars->dq_full);
         umma_commit(&bars->dsq_done);
@@ -322,8 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit(&bars->dp_full);
         }
       }
-      __syncwarp();
+      umma_commit(&bars->mma_done);
+      pa.mark(6);
+      pa.flush(g_trace_smem, 13);
+#ifdef SKR_PHASE_ACCT
+      if (g_trace_smem != nullptr) g_trace_smem[13 * 8 + 7] = (unsigned long long)n_steps;
+#endif
     }
+    __syncwarp();
   } else if (warp < 8) {
     // ================= two compute warpgroups: thread = key row, warpgroup = half of the query columns
     const int j = (warp % 4) * 32 + lane;
@@ -335,6 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sAux = smem_u32(aux);
     const int wg = warp / 4;
     StepIter it(qt_first, qt_last);
+    // 0 wait Q/dO + S, 1 load S, 2 exp + mask, 3 wait dV done, 4 store P^T, 5 wait dP, 6 dS math, 7 store dS
+    PhaseAcct pa;
+    pa.start();
     for (int n = 0; n < n_steps; ++n, it.next()) {
       const int st = n % C::kStages;
       const int qp_base = q_pos + it.qt * BQ + col0;        // position of this warpgroup's first query
@@ -342,20 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1);
       const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (C::kStages * BQ + st * BQ + col0) * 4;
       mbar_wait(&bars->s_full, n & 1);
+      pa.mark(0);
       if (threadIdx.x == 0) trace(10);
       tc_fence_after();
-      if (kSkipMath && g_skip_math) {
-        tc_fence_before();
-        mbar_arrive(&bars->s_free);
-        if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);
-        mbar_arrive(&bars->p_full);
-        mbar_wait(&bars->dp_full, n & 1);
-        mbar_arrive(&bars->dp_free);
-        if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);
-        mbar_arrive(&bars->ds_full);
-        if (threadIdx.x == 0) trace(13);
-        continue;
-      }
       float p[H];
 #pragma unroll
       for (int c = 0; c < H; c += 32) {
@@ -367,23 +367,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars->s_free);                   // S TMEM may be overwritten by S(n+1)
+      pa.mark(1);
       const float2 sl2_2 = make_float2(sl2, sl2);
 #pragma unroll
       for (int i = 0; i < H; i += 4) {
         const float4 l4 = ld_shared_f4(a_lse + i * 4);     // -lse2 is folded: p * sl2 - lse2
         const float2 e0 = ffma2(make_float2(p[i], p[i + 1]), sl2_2, make_float2(-l4.x, -l4.y));
         const float2 e1 = ffma2(make_float2(p[i + 2], p[i + 3]), sl2_2, make_float2(-l4.z, -l4.w));
-        p[i + 0] = ex2(e0.x);
-        p[i + 1] = ex2(e0.y);
-        p[i + 2] = ex2(e1.x);
-        p[i + 3] = ex2(e1.y);
+        // element (i % 8) < kPolyPer8 on the FMA pipe, the rest on MUFU
+        p[i + 0] = (i % 8) + 0 < kPolyPer8 ? ex2_poly(e0.x) : ex2(e0.x);
+        p[i + 1] = (i % 8) + 1 < kPolyPer8 ? ex2_poly(e0.y) : ex2(e0.y);
+        p[i + 2] = (i % 8) + 2 < kPolyPer8 ? ex2_poly(e1.x) : ex2(e1.x);
+        p[i + 3] = (i % 8) + 3 < kPolyPer8 ? ex2_poly(e1.y) : ex2(e1.y);
       }
       if (diag) {
 #pragma unroll
         for (int i = 0; i < H; ++i)
           if (kvp > qp_base + i) p[i] = 0.f;               // causal (invalid queries: lse2 = +inf -> 0)
       }
+      pa.mark(2);
       if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T TMEM columns free
+      pa.mark(3);
       tc_fence_after();
       {
         uint32_t pk[H / 2];
@@ -395,29 +399,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->p_full);
       if (threadIdx.x == 0) trace(11);
+      pa.mark(4);
       mbar_wait(&bars->dp_full, n & 1);
       if (threadIdx.x == 0) trace(12);
+      pa.mark(5);
       tc_fence_after();
+      {
+        // dP^T loads: all in flight under one wait where the registers allow (d = 128: 32 columns per
+        // warpgroup); d = 64 holds 64 P values already, so one 32-column chunk at a time
+        constexpr int kBatch = H <= 32 ? H / 32 : 1;
 #pragma unroll
-      for (int c = 0; c < H; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + C::tDP + col0 + c, r);
-        tmem_wait_ld();
-        if (c + 32 >= H) {
-          tc_fence_before();
-          mbar_arrive(&bars->dp_free);              // dP TMEM may be overwritten by dP(n+1)
-        }
+        for (int cb = 0; cb < H; cb += 32 * kBatch) {
+          uint32_t r[kBatch][32];
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
-          const float2 t0 = fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(-d4.x, -d4.y));
-          const float2 t1 = fadd2(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])),
-                                  make_float2(-d4.z, -d4.w));
-          const float2 s0 = fmul2(make_float2(p[c + i], p[c + i + 1]), t0);
-          const float2 s1 = fmul2(make_float2(p[c + i + 2], p[c + i + 3]), t1);
-          p[c + i + 0] = s0.x, p[c + i + 1] = s0.y, p[c + i + 2] = s1.x, p[c + i + 3] = s1.y;
+          for (int b = 0; b < kBatch; ++b) tmem_ld32(tmem + lane_base + C::tDP + col0 + cb + 32 * b, r[b]);
+          tmem_wait_ld();
+          if (cb + 32 * kBatch >= H) {
+            tc_fence_before();
+            mbar_arrive(&bars->dp_free);            // dP TMEM may be overwritten by dP(n+1)
+          }
+#pragma unroll
+          for (int b = 0; b < kBatch; ++b)
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const int c = cb + 32 * b;
+              const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
+              const float2 t0 = fadd2(make_float2(__uint_as_float(r[b][i]), __uint_as_float(r[b][i + 1])),
+                                      make_float2(-d4.x, -d4.y));
+              const float2 t1 = fadd2(make_float2(__uint_as_float(r[b][i + 2]), __uint_as_float(r[b][i + 3])),
+                                      make_float2(-d4.z, -d4.w));
+              const float2 s0 = fmul2(make_float2(p[c + i], p[c + i + 1]), t0);
+              const float2 s1 = fmul2(make_float2(p[c + i + 2], p[c + i + 3]), t1);
+              p[c + i + 0] = s0.x, p[c + i + 1] = s0.y, p[c + i + 2] = s1.x, p[c + i + 3] = s1.y;
+            }
         }
       }
+      pa.mark(6);
       if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem / TMEM free
       tc_fence_after();
       {
@@ -436,10 +453,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->ds_full);
+      pa.mark(7);
       if (threadIdx.x == 0) trace(13);
     }
+    if (lane == 0) pa.flush(g_trace_smem, warp);
     // ---- dK, dV epilogue: warpgroup 0 stores dK, warpgroup 1 stores dV
-    mbar_wait(&bars->dsq_done, (n_steps - 1) & 1);
+    mbar_wait(&bars->mma_done, 0);   // single-phase: no parity ambiguity however far a role ran ahead
     tc_fence_after();
     const bool valid = kvp < k_len;
     const size_t row = (size_t)(kst + kvp) * a.hkv + g;
@@ -479,29 +498,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kBoxes = D / 32;                 // 32-column fp32 boxes
     constexpr int kBoxBytes = BQ * 128;
     StepIter it(qt_first, qt_last);
+    PhaseAcct pa;   // 0 wait dQ, 1 wait smem tile free, 2 TMEM -> smem, 3 issue reduce
+    pa.start();
     for (int n = 0; n < n_steps; ++n, it.next()) {
       const int h = g * grp + it.hi, q0 = it.qt * BQ;
       mbar_wait(&bars->dq_full, n & 1);
+      pa.mark(0);
       if (t == 0) trace(20);
       tc_fence_after();
-      if (kSkipMath && g_skip_math) {
-        mbar_arrive(&bars->dq_empty);
-        continue;
-      }
       // the previous step's reduce must have finished reading the smem tile
       if (warp == 8 && elect_one()) bulk_wait_read<0>();
       named_bar_sync(1, 128);
+      pa.mark(1);
       if (D == 128) {
-        // dQ^T: lane = feature t, columns = queries of the step
+        // dQ^T: lane = feature t, columns = queries of the step. Element (q, t) of a SW128 box sits at
+        // q * 128 + (((t / 4) ^ (q % 8)) * 16) + (t % 4) * 4: eight per-thread offsets (q % 8) plus
+        // compile-time q * 128 immediates, one STS per element. (Direct red.global from registers
+        // instead of the smem tile + TMA reduce was measured 1.5x slower for the whole kernel.)
+        uint32_t off[8];
 #pragma unroll
-        for (int c = 0; c < BQ; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tmem + lane_base + C::tDQ + c, r);
-          tmem_wait_ld();
+        for (int m = 0; m < 8; ++m)
+          off[m] = sDQ + (t / 32) * kBoxBytes + ((((t % 32) >> 2) ^ m) << 4) + (t & 3) * 4;
+        uint32_t r[BQ / 32][32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            st_shared_f32(sDQ + (t / 32) * kBoxBytes + sw128_off_f32(c + i, t % 32), __uint_as_float(r[i]) * a.scale);
-        }
+        for (int c = 0; c < BQ; c += 32) tmem_ld32(tmem + lane_base + C::tDQ + c, r[c / 32]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < BQ; ++q)
+          st_shared_f32(off[q % 8] + q * 128, __uint_as_float(r[q / 32][q % 32]) * a.scale);
       } else {
         // dQ: lane = query row t, columns = features
 #pragma unroll
@@ -518,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars->dq_empty);                // TMEM dQ columns may be overwritten
+      pa.mark(2);
       if (t == 0) trace(21);
       fence_async_smem();
       named_bar_sync(1, 128);
@@ -530,7 +555,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
+      pa.mark(3);
     }
+    if (lane == 0) pa.flush(g_trace_smem, warp);
     if (warp == 8 && elect_one()) bulk_wait<0>();
   }
   tc_fence_before();
@@ -643,16 +670,30 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
         !make_tmap_2d(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n_q_rows, qcols, qcols, bq, 32, true))
       return fail(SKR_E_CUDA, "attn bwd: tensor map encode failed");
     dim3 grid(a.hkv, a.n_tiles);
+    // share of exponentials on the FMA pipe; SKR_BWD_POLY (0-3) overrides for sweeps
+    static int poly = [] {
+      const char* e = getenv("SKR_BWD_POLY");
+      const int v = e ? atoi(e) : -1;
+      return (v >= 0 && v <= 3) ? v : -1;
+    }();
+    // measured (profiles/bwd_period.py, S = 16K): no gain at d=64, a loss at d=128 -> MUFU only
+    const int pp = poly >= 0 ? poly : 0;
+    auto launch = [&](auto kern, int smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kern<<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv, accumulate, dq_acc);
+    };
     if (d == 128) {
       constexpr int smem = bwd::Cfg<128>::kSmem;
-      cudaFuncSetAttribute(bwd::attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      bwd::attn_bwd_kernel<128><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv,
-                                                                   accumulate);
+      if (pp == 0) launch(bwd::attn_bwd_kernel<128, 0>, smem);
+      else if (pp == 1) launch(bwd::attn_bwd_kernel<128, 1>, smem);
+      else if (pp == 2) launch(bwd::attn_bwd_kernel<128, 2>, smem);
+      else launch(bwd::attn_bwd_kernel<128, 3>, smem);
     } else {
       constexpr int smem = bwd::Cfg<64>::kSmem;
-      cudaFuncSetAttribute(bwd::attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      bwd::attn_bwd_kernel<64><<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv,
-                                                                  accumulate);
+      if (pp == 0) launch(bwd::attn_bwd_kernel<64, 0>, smem);
+      else if (pp == 1) launch(bwd::attn_bwd_kernel<64, 1>, smem);
+      else if (pp == 2) launch(bwd::attn_bwd_kernel<64, 2>, smem);
+      else launch(bwd::attn_bwd_kernel<64, 3>, smem);
     }
     if (skr_status e = launch_status("attn_bwd_kernel")) return e;
   }

@@ -71,35 +71,6 @@ __device__ __forceinline__ void trace_sm(int, int) {}
 __device__ __forceinline__ void trace_smw(int, int) {}
 #endif
 
-// Phase accounting (SKR_PHASE_ACCT builds): per-warp cycle totals of each phase of the loop kept in
-// registers and written once at the end (block (0, 0) only) - no events on the path, so the
-// warps are not perturbed the way per-event traces perturb them.
-struct PhaseAcct {
-#ifdef SKR_PHASE_ACCT
-  long long t, acc[8];
-  __device__ __forceinline__ void start() {
-    t = clock64();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0;
-  }
-  __device__ __forceinline__ void mark(int k) {
-    const long long n = clock64();
-    acc[k] += n - t;
-    t = n;
-  }
-  __device__ __forceinline__ void flush(int slot) {
-    unsigned long long* b = g_trace_smem;
-    if (b != nullptr)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) b[slot * 8 + k] = (unsigned long long)acc[k];
-  }
-#else
-  __device__ __forceinline__ void start() {}
-  __device__ __forceinline__ void mark(int) {}
-  __device__ __forceinline__ void flush(int) {}
-#endif
-};
-
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -210,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
       }
     }
     pa.mark(1);
-    if (lane == 0) pa.flush(8);
+    if (lane == 0) pa.flush(g_trace_smem, 8);
   } else if (warp == 9) {
     // ================= MMA issuer: ONE elected thread runs the whole loop. Measured (profiles/
     // umma_probe.py): the tensor pipe buffers only about one MMA ahead of the issuing thread, and
@@ -317,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         }
       }
       pa.mark(3);
-      pa.flush(9);
+      pa.flush(g_trace_smem, 9);
     }
     __syncwarp();
   } else {
@@ -445,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         pa.mark(4);
         if (lane == 0) trace_smw(30 + 20 * s + 4, j | (warp % 4) << 6);
       }
-      if (lane == 0) pa.flush(warp);
+      if (lane == 0) pa.flush(g_trace_smem, warp);
       // ---- epilogue: O / l -> bf16, LSE
       mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
       tc_fence_after();

@@ -324,6 +324,37 @@ __device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Phase accounting (SKR_PHASE_ACCT builds): per-warp cycle totals of each phase of the loop kept in
+// registers and written once at the end (the kernel passes its traced block's buffer) - no events on the path, so the
+// warps are not perturbed the way per-event traces perturb them.
+struct PhaseAcct {
+#ifdef SKR_PHASE_ACCT
+  long long t, acc[8];
+  __device__ __forceinline__ void start() {
+    t = clock64();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0;
+  }
+  __device__ __forceinline__ void mark(int k) {
+    const long long n = clock64();
+    acc[k] += n - t;
+    t = n;
+  }
+  __device__ __forceinline__ void flush(unsigned long long* b, int slot) {
+    if (b != nullptr)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) b[slot * 8 + k] = (unsigned long long)acc[k];
+  }
+#else
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush(unsigned long long*, int) {}
+#endif
+};
+
+__device__ __forceinline__ void red_add_f32(float* addr, float a) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
