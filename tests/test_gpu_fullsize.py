@@ -1,0 +1,140 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the same
+plan, RankStep tables and C-ABI calls), on outputs the fp64 oracle can compute one by one.
+
+Full batches are far beyond what the naive oracle finishes in seconds (C2's 32K sequence alone is
+~1e12 fp64 flop), so each check is on a SAMPLE whose oracle values are exact restrictions of the
+plain definition:
+  * query row i of sequence s: O_i, LSE_i and dQ_i depend only on q_i, do_i and keys 0..i
+    -> oracle.attn_fwd / attn_bwd on the single row with q_pos = i;
+  * key rows j >= j0: dK_j, dV_j receive contributions only from queries i >= j, all inside the
+    tail [j0, S) -> oracle.attn_bwd on the tail query block with q_pos = j0 (its dK/dV rows >= j0
+    are the full-sequence values);
+  * every sequence of <= 512 tokens: all outputs, whole.
+Inputs are the seeded per-sequence tensors of synth.seq_tensors (bf16-rounded), placed into each
+rank's rank-natural source buffer exactly as a DataLoader would hand them over (R38).
+Tolerance: R34' bf16 bound (tests/attn_harness.tol_ok).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.attention import attn_bwd, attn_fwd  # noqa: E402
+from oracle.cost_model import Model  # noqa: E402
+from oracle.schedule import plan as oracle_plan  # noqa: E402
+from synth import CONFIGS, seq_tensors  # noqa: E402
+from tests.attn_harness import tol_ok  # noqa: E402
+
+SHORT_WHOLE = 512
+N_ROWS = 6          # random query rows per sampled long sequence (plus fixed edge rows)
+TAIL = 192          # key rows checked at the end of each sampled long sequence
+
+
+def _launch(cfg_name, seed):
+    """Plan + run one fwd+bwd step of the whole batch as bench.py does; returns per-seq lookups."""
+    from paper_2505_19609_b200 import skrull as sk
+    from paper_2505_19609_b200.runtime import RankStep, loopback_step, rank_natural_rows
+    cfg = CONFIGS[cfg_name]
+    lens = cfg.lengths(seed)
+    shp, N, C = cfg.shape, cfg.cp, cfg.bucket
+    shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
+    p = sk.skr_plan(lens, C, N, 1, shp.hidden, shp.kv_hidden)
+    ref = oracle_plan([int(x) for x in lens], C, N, 1, Model(shp.hidden, shp.kv_hidden))
+    assert list(p["assign"]) == list(ref.assign)                    # bit-exact plan at full size
+    # per-sequence device tensors (bf16), generated once
+    dev = {}
+    for k, S in enumerate(lens):
+        x = seq_tensors(seed, k, int(S), shp.hq, shp.hkv, shp.d)
+        dev[k] = {n: torch.from_numpy(a).to("cuda", torch.bfloat16) for n, a in x.items()}
+        del x
+    loc = {}       # (seq, pos) lookup: seq -> list of (micro-batch, rank, packed row start, q_pos, q_len)
+    runs = []
+    for j in range(int(p["n_mb_per_dp"][0])):
+        idx = np.nonzero(p["mb_of_seq"] == j)[0]
+        ml, ma = lens[idx], p["assign"][idx]
+        ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
+        srcs = {}
+        for name in ("q", "k", "v", "do"):
+            srcs[name] = []
+            for r in range(N):
+                parts = [dev[int(idx[kk])][name][lo:hi] for kk, lo, hi in rank_natural_rows(ml, ma, N, r)]
+                srcs[name].append(torch.cat(parts) if parts else
+                                  torch.zeros(1, dev[0][name].shape[1], shp.d, device="cuda", dtype=torch.bfloat16))
+        if N == 1:
+            side = torch.cuda.Stream(priority=-1)
+            ranks[0].forward(srcs["q"][0], srcs["k"][0], srcs["v"][0], None, side)
+            ranks[0].backward(srcs["do"][0], None, side)
+        else:
+            loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+        torch.cuda.synchronize()
+        for r, rs in enumerate(ranks):
+            pr = rs.pr
+            for i in range(pr["n_seg"]):
+                a, b = int(pr["cu_seqlens_q"][i]), int(pr["cu_seqlens_q"][i + 1])
+                s = int(idx[pr["seg_seq"][i]])
+                loc.setdefault(s, []).append((len(runs), r, a, int(pr["q_pos"][i]), b - a))
+        runs.append(ranks)
+        del srcs
+    return cfg, lens, runs, loc
+
+
+def _rows(runs, loc, s, positions, key):
+    """Gather output `key` ('o', 'dq', 'dk', 'dv', 'lse') of sequence s at the given positions."""
+    out = []
+    for t in positions:
+        for m, r, a, qp, ql in loc[s]:
+            if qp <= t < qp + ql:
+                rs = runs[m][r]
+                row = a + (t - qp)
+                out.append(rs.lse[:, row].float().cpu().numpy() if key == "lse"
+                           else getattr(rs, key)[row].float().cpu().numpy())
+                break
+        else:
+            raise AssertionError(f"seq {s} position {t} not covered by any segment")
+    return np.stack(out)
+
+
+def _check(name, got, ref, where):
+    ok, err, bound = tol_ok(got, ref, False)
+    assert ok, f"{name} {where}: err {err} > {bound}"
+
+
+@pytest.mark.parametrize("cfg_name", ["C2", "C5n1", "C3n2"])
+def test_fullsize_sampled(cfg_name):
+    cfg, lens, runs, loc = _launch(cfg_name, 0)
+    rng = np.random.default_rng(1234)
+    order = np.argsort(lens, kind="stable")
+    longest = int(order[-1])
+    sampled = [longest] + [int(k) for k in rng.choice(order[:-1], size=2, replace=False) if lens[k] > SHORT_WHOLE]
+    shorts = [int(k) for k in order if lens[k] <= SHORT_WHOLE][:24]
+    shp = cfg.shape
+    checked = 0
+    for s in shorts:
+        S = int(lens[s])
+        x = seq_tensors(0, s, S, shp.hq, shp.hkv, shp.d)
+        O, L = attn_fwd(x["q"], x["k"], x["v"])
+        dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
+        pos = range(S)
+        for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
+            _check(key, _rows(runs, loc, s, pos, key), ref, f"{cfg_name} short seq {s} (S={S})")
+        assert np.abs(_rows(runs, loc, s, pos, "lse").T - L).max() <= 2e-2
+        checked += 1
+    for s in sampled:
+        S = int(lens[s])
+        x = seq_tensors(0, s, S, shp.hq, shp.hkv, shp.d)
+        rows = sorted(set([0, 1, 127, 128, S // 2, S - 1] + [int(v) for v in rng.integers(0, S, N_ROWS)]))
+        for i in rows:
+            O, L = attn_fwd(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], q_pos=i)
+            dQ, _, _ = attn_bwd(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], x["do"][i:i + 1], q_pos=i)
+            where = f"{cfg_name} seq {s} (S={S}) row {i}"
+            _check("o", _rows(runs, loc, s, [i], "o"), O, where)
+            _check("dq", _rows(runs, loc, s, [i], "dq"), dQ, where)
+            assert np.abs(_rows(runs, loc, s, [i], "lse").T - L).max() <= 2e-2, where
+        j0 = max(0, S - TAIL)
+        _, dK, dV = attn_bwd(x["q"][j0:], x["k"], x["v"], x["do"][j0:], q_pos=j0)
+        tail = range(j0, S)
+        _check("dk", _rows(runs, loc, s, tail, "dk"), dK[j0:], f"{cfg_name} seq {s} (S={S}) key tail")
+        _check("dv", _rows(runs, loc, s, tail, "dv"), dV[j0:], f"{cfg_name} seq {s} (S={S}) key tail")
+        checked += 1
+    assert checked >= 3
