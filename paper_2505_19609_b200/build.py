@@ -21,8 +21,12 @@ CSRC = os.path.join(PKG, "csrc")
 # SKR_KERNEL_TRACE=1: instrumented debug build into its own objects / library (load it with
 # SKR_LIB_PATH=.../libskrull_trace.so); the production library never carries the trace hooks
 _TRACE = bool(os.environ.get("SKR_KERNEL_TRACE"))   # "1": event timeline, "phase": phase accounting
-BUILD = os.path.join(ROOT, "build_trace" if _TRACE else "build")
-LIB = os.path.join(PKG, "libskrull_trace.so" if _TRACE else "libskrull.so")
+# SKR_VARIANT=<name> SKR_VARIANT_DEFS="-DX ...": an experiment build (build_<name>/, libskrull_<name>.so) for
+# A/B timing on the same box (profiles/ab.sh); never the production library
+_VARIANT = os.environ.get("SKR_VARIANT", "")
+_SUFFIX = "_trace" if _TRACE else (f"_{_VARIANT}" if _VARIANT else "")
+BUILD = os.path.join(ROOT, "build" + _SUFFIX)
+LIB = os.path.join(PKG, f"libskrull{_SUFFIX}.so")
 INCLUDE = os.path.join(ROOT, "include")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
@@ -50,6 +54,8 @@ def _flags():
         trace.append("-DSKR_PHASE_ACCT" if os.environ["SKR_KERNEL_TRACE"] == "phase" else "-DSKR_KERNEL_TRACE")
     if _TRACE and os.environ.get("SKR_TRACE_SOFTMAX"):
         trace.append("-DSKR_TRACE_SOFTMAX")
+    if _VARIANT:
+        trace += os.environ.get("SKR_VARIANT_DEFS", "").split()
     cu = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", *trace,
           "--expt-relaxed-constexpr", "-Xptxas", "-v", *inc]
     cc = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",

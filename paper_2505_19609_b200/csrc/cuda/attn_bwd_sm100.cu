@@ -371,7 +371,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 sl2_2 = make_float2(sl2, sl2);
 #pragma unroll
       for (int i = 0; i < H; i += 4) {
+#ifdef SKR_EXP_NO_LDS   // timing experiment only (wrong results): LSE / D loads removed
+        const float4 l4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
+#else
         const float4 l4 = ld_shared_f4(a_lse + i * 4);     // -lse2 is folded: p * sl2 - lse2
+#endif
         const float2 e0 = ffma2(make_float2(p[i], p[i + 1]), sl2_2, make_float2(-l4.x, -l4.y));
         const float2 e1 = ffma2(make_float2(p[i + 2], p[i + 3]), sl2_2, make_float2(-l4.z, -l4.w));
         // element (i % 8) < kPolyPer8 on the FMA pipe, the rest on MUFU
@@ -423,7 +427,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const int c = cb + 32 * b;
+#ifdef SKR_EXP_NO_LDS
+              const float4 d4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
+#else
               const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
+#endif
               const float2 t0 = fadd2(make_float2(__uint_as_float(r[b][i]), __uint_as_float(r[b][i + 1])),
                                       make_float2(-d4.x, -d4.y));
               const float2 t1 = fadd2(make_float2(__uint_as_float(r[b][i + 2]), __uint_as_float(r[b][i + 3])),
@@ -506,6 +514,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       pa.mark(0);
       if (t == 0) trace(20);
       tc_fence_after();
+#if defined(SKR_EXP_NO_DQ) || defined(SKR_EXP_DQ_RED)   // timing experiments
+      if (D == 128) {
+        uint32_t r[BQ / 32][32];
+#pragma unroll
+        for (int c = 0; c < BQ; c += 32) tmem_ld32(tmem + lane_base + C::tDQ + c, r[c / 32]);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bars->dq_empty);
+#ifdef SKR_EXP_DQ_RED
+        const int nv = min(BQ, q_len - q0);
+        float* base = dq_acc + ((size_t)(cu0 + q0) * a.hq + h) * D + t;
+#pragma unroll
+        for (int q = 0; q < BQ; ++q)
+          if (q < nv) red_add_f32(base + (size_t)q * a.hq * D, __uint_as_float(r[q / 32][q % 32]) * a.scale);
+#else
+        if (__uint_as_float(r[0][0]) == 1234.5f) dq_acc[t] = 0.f;
+#endif
+        continue;
+      }
+#endif
       // the previous step's reduce must have finished reading the smem tile
       if (warp == 8 && elect_one()) bulk_wait_read<0>();
       named_bar_sync(1, 128);
@@ -674,7 +702,7 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
     static int poly = [] {
       const char* e = getenv("SKR_BWD_POLY");
       const int v = e ? atoi(e) : -1;
-      return (v >= 0 && v <= 3) ? v : -1;
+      return (v >= 0 && v <= 4) ? v : -1;
     }();
     // measured (profiles/bwd_period.py, S = 16K): no gain at d=64, a loss at d=128 -> MUFU only
     const int pp = poly >= 0 ? poly : 0;
@@ -687,13 +715,15 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
       if (pp == 0) launch(bwd::attn_bwd_kernel<128, 0>, smem);
       else if (pp == 1) launch(bwd::attn_bwd_kernel<128, 1>, smem);
       else if (pp == 2) launch(bwd::attn_bwd_kernel<128, 2>, smem);
-      else launch(bwd::attn_bwd_kernel<128, 3>, smem);
+      else if (pp == 3) launch(bwd::attn_bwd_kernel<128, 3>, smem);
+      else launch(bwd::attn_bwd_kernel<128, 4>, smem);
     } else {
       constexpr int smem = bwd::Cfg<64>::kSmem;
       if (pp == 0) launch(bwd::attn_bwd_kernel<64, 0>, smem);
       else if (pp == 1) launch(bwd::attn_bwd_kernel<64, 1>, smem);
       else if (pp == 2) launch(bwd::attn_bwd_kernel<64, 2>, smem);
-      else launch(bwd::attn_bwd_kernel<64, 3>, smem);
+      else if (pp == 3) launch(bwd::attn_bwd_kernel<64, 3>, smem);
+      else launch(bwd::attn_bwd_kernel<64, 4>, smem);
     }
     if (skr_status e = launch_status("attn_bwd_kernel")) return e;
   }

@@ -491,7 +491,7 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   static int poly = [] {
     const char* e = getenv("SKR_FWD_POLY");
     const int v = e ? atoi(e) : -1;
-    return (v >= 0 && v <= 3) ? v : -1;
+    return (v >= 0 && v <= 4) ? v : -1;
   }();
   // measured (profiles/fwd_period.py, S = 32K): d=64 best at 2/8, d=128 at 1/8; beyond that the
   // polynomial's FMA / ALU instructions cost more issue slots than the MUFU time they save
@@ -506,7 +506,8 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
       case 0: launch(fwd::attn_fwd_kernel<128, 0>, smem); break;
       case 1: launch(fwd::attn_fwd_kernel<128, 1>, smem); break;
       case 2: launch(fwd::attn_fwd_kernel<128, 2>, smem); break;
-      default: launch(fwd::attn_fwd_kernel<128, 3>, smem); break;
+      case 3: launch(fwd::attn_fwd_kernel<128, 3>, smem); break;
+      default: launch(fwd::attn_fwd_kernel<128, 4>, smem); break;
     }
   } else if (d == 64) {
     constexpr int smem = fwd::Cfg<64>::kSmem;
@@ -514,7 +515,8 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
       case 0: launch(fwd::attn_fwd_kernel<64, 0>, smem); break;
       case 1: launch(fwd::attn_fwd_kernel<64, 1>, smem); break;
       case 2: launch(fwd::attn_fwd_kernel<64, 2>, smem); break;
-      default: launch(fwd::attn_fwd_kernel<64, 3>, smem); break;
+      case 3: launch(fwd::attn_fwd_kernel<64, 3>, smem); break;
+      default: launch(fwd::attn_fwd_kernel<64, 4>, smem); break;
     }
   } else {
     return fail(SKR_E_UNSUPPORTED, "bf16 attention supports d in {64, 128}");

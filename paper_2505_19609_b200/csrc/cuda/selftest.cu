@@ -290,6 +290,15 @@ __global__ void mufu_kernel(int iters, int mode, long long* cycles, float* sink)
         x[i + 1] = ex2(xx.y);
         acc = fadd2(acc, make_float2(x[i], x[i + 1]));
         pk ^= pack_bf16(x[i], x[i + 1]);
+      } else if (mode == 2 || mode == 3) {
+        // packed half-precision ex2: two results per instruction (mode 2 f16x2, mode 3 bf16x2)
+        uint32_t h = __float_as_uint(x[i]);
+        if (mode == 2)
+          asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+        else
+          asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h));
+        x[i] = __uint_as_float(h ^ 0x80008000u);
+        x[i + 1] = x[i];
       } else {
         x[i] = ex2(x[i] * -0.5f);
         x[i + 1] = ex2(x[i + 1] * -0.5f);
