@@ -71,8 +71,17 @@ struct Cfg {
   static constexpr int kOffDO = kOffQ + kStages * kQBytes; // [kStages]
   static constexpr int kOffDS = kOffDO + kStages * kQBytes;
   static constexpr int kOffDQ = kOffDS + kPBytes;
-  static constexpr int kOffAux = kOffDQ + kDQBytes;       // lse2[kStages][BQ], dd[kStages][BQ] fp32
-  static constexpr int kOffBar = kOffAux + 2 * kStages * BQ * 4;
+  // d = 64: -LSE/scale and -D enter the S^T / dP^T accumulators through one K = 16 MMA each
+  // (ones[128 x 16] x split[16 x BQ], the value as a 3-term bf16 split in k-rows 0-2), so the
+  // compute warps never broadcast-load per-query values from shared memory (those loads were half
+  // of all LSU shared traffic, profiles/r01_experiments.md). d = 128 keeps the smem rows.
+  static constexpr bool kInit = D == 64;
+  static constexpr int kInitBytes = 16 * BQ * 2;          // [16 k-rows][BQ] bf16, MN-major SW128 boxes
+  static constexpr int kOnesBytes = 16 * BN * 2;          // [16 k-rows][BN] bf16 ones, MN-major
+  static constexpr int kOffAux = kOffDQ + kDQBytes;       // kInit: [kStages][2] init tiles + ones;
+                                                          // else lse2[kStages][BQ], dd[kStages][BQ] fp32
+  static constexpr int kAuxBytes = kInit ? kStages * 2 * kInitBytes + kOnesBytes : 2 * kStages * BQ * 4;
+  static constexpr int kOffBar = kOffAux + kAuxBytes;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   // TMEM columns. P^T and dS^T (bf16 pairs) are the A operands of dV / dK straight from TMEM.
   //  d = 128: S^T[0,64) dP^T[64,128) dQ^T[128,192) P^T[192,224) dS^T[224,256) dV[256,384) dK[384,512)
@@ -152,6 +161,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   trace_init();
+  if (C::kInit) {
+    // zero the init tiles (k-rows 3-15 stay zero) and fill the ones tile, then hand them to the
+    // async proxy (the MMA reads them)
+    uint4* z = reinterpret_cast<uint4*>(smem + C::kOffAux);
+    constexpr int nz = C::kStages * 2 * C::kInitBytes / 16, no = C::kOnesBytes / 16;
+    for (int i = threadIdx.x; i < nz + no; i += kThreads)
+      z[i] = i < nz ? make_uint4(0u, 0u, 0u, 0u) : make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    fence_async_smem();
+  }
   if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -176,14 +194,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     // overlaps the wait for the stage to free up instead of delaying the compute warpgroups.
     constexpr int kPer = BQ / 32;
     float pl[kPer], pd[kPer];
+    const float inv_scale = 1.f / a.scale;
     auto fetch = [&](const StepIter& s_) {
       const int h = g * grp + s_.hi, q0 = s_.qt * BQ, nv = min(BQ, q_len - q0);
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         const int i = lane + 32 * u;
         const size_t off = (size_t)h * a.ld_lse + cu0 + q0 + i;
-        pl[u] = i < nv ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
-        pd[u] = i < nv ? Dbuf[off] : 0.f;
+        if (C::kInit) {   // accumulator init values: S^T - LSE/scale, dP^T - D
+          pl[u] = i < nv ? -lse[off] * inv_scale : -1e30f;             // p = 0 for invalid queries
+          pd[u] = i < nv ? -Dbuf[off] : 0.f;
+        } else {
+          pl[u] = i < nv ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
+          pd[u] = i < nv ? Dbuf[off] : 0.f;
+        }
       }
     };
     StepIter it(qt_first, qt_last);
@@ -201,10 +225,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                       h * D + c * 64, cu0 + q0);
         }
       }
+      if (C::kInit) {
+        // 3-term bf16 split (hi + mid + lo carries ~24 bits) into k-rows 0-2 of column n
+        const uint32_t tl = smem_u32(smem + C::kOffAux + (st * 2) * C::kInitBytes);
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        aux[st * BQ + lane + 32 * u] = pl[u];
-        aux[C::kStages * BQ + st * BQ + lane + 32 * u] = pd[u];
+        for (int u = 0; u < kPer; ++u) {
+          const int n = lane + 32 * u;
+          const uint32_t col = (n / 64) * (16 * 128);
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            float v = w == 0 ? pl[u] : pd[u];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              const __nv_bfloat16 b = __float2bfloat16_rn(v);
+              v -= __bfloat162float(b);
+              st_shared_u16(tl + w * C::kInitBytes + col + sw128_off(k, n % 64), __bfloat16_as_ushort(b));
+            }
+          }
+        }
+        fence_async_smem();
+      } else {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          aux[st * BQ + lane + 32 * u] = pl[u];
+          aux[C::kStages * BQ + st * BQ + lane + 32 * u] = pd[u];
+        }
       }
       __syncwarp();
       mbar_arrive(&bars->qdo_full[st]);
@@ -226,12 +271,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dQmn = sdesc_sw128(sQ, BQ * 128, 1024), dDOmn = sdesc_sw128(sDO, BQ * 128, 1024);
     const uint64_t dKmn = sdesc_sw128(sK, BN * 128, 1024), dDSmn = sdesc_sw128(sDS, BN * 128, 1024);
     const uint64_t dK0 = sdesc_sw128(sK, 0, 1024), dDS0 = sdesc_sw128(sDS, 0, 1024);
-    auto issue_t = [&](uint64_t a_desc, uint64_t b_desc, uint32_t tcol) {
+    // kInit: ones[BN x 16] x init[16 x BQ] (both MN-major SW128, LBO = 64-column box stride) writes
+    // -LSE/scale (S^T) or -D (dP^T) into every lane of the accumulator; the GEMM then accumulates
+    const uint32_t id_init = idesc_bf16_f32(BN, BQ, 1, 1);
+    const uint64_t dOnes = sdesc_sw128(smem_u32(smem + C::kOffAux + C::kStages * 2 * C::kInitBytes), 16 * 128, 1024);
+    const uint64_t dInit = sdesc_sw128(smem_u32(smem + C::kOffAux), 16 * 128, 1024);
+    auto issue_t = [&](uint64_t a_desc, uint64_t b_desc, uint32_t tcol, int init_tile) {
+      if (C::kInit)
+        umma_f16(tmem + tcol, dOnes, dInit + ((uint32_t)(init_tile * C::kInitBytes) >> 4), id_init, 0);
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint32_t ao = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
         const uint32_t bo = ((k / 4) * (BQ * 128) + (k % 4) * 32) >> 4;
-        umma_f16(tmem + tcol, a_desc + ao, b_desc + bo, id_sdp, k > 0);
+        umma_f16(tmem + tcol, a_desc + ao, b_desc + bo, id_sdp, C::kInit || k > 0);
       }
     };
     // dV / dK: A = P^T or dS^T from TMEM (k-step = 16 queries = 8 packed columns of one warpgroup
@@ -264,9 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_sleep(&bars->kv_full, 0);
       mbar_wait_sleep(&bars->qdo_full[0], 0);
       tc_fence_after();
-      issue_t(dK, dQ, C::tS);
+      issue_t(dK, dQ, C::tS, 0);
       umma_commit(&bars->s_full);
-      issue_t(dV, dDO, C::tDP);
+      issue_t(dV, dDO, C::tDP, 1);
       umma_commit(&bars->dp_full);
       // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its
       // own columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows
@@ -284,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pa.mark(1);
           trace(2);
           tc_fence_after();
-          issue_t(dK, dQ + st1 * qstage, C::tS);
+          issue_t(dK, dQ + st1 * qstage, C::tS, 2 * st1);
           umma_commit(&bars->s_full);
         }
         pa.mark(6);
@@ -300,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pa.mark(3);
           if (more) {
             tc_fence_after();
-            issue_t(dV, dDO + st1 * qstage, C::tDP);
+            issue_t(dV, dDO + st1 * qstage, C::tDP, 2 * st1 + 1);
             umma_commit(&bars->dp_full);
           }
         }
@@ -320,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bars->dsq_done);
         umma_commit(&bars->qdo_empty[st]);
         if (C::kDSAlias && more) {
-          issue_t(dV, dDO + st1 * qstage, C::tDP);
+          issue_t(dV, dDO + st1 * qstage, C::tDP, 2 * st1 + 1);
           umma_commit(&bars->dp_full);
         }
       }
@@ -371,13 +423,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 sl2_2 = make_float2(sl2, sl2);
 #pragma unroll
       for (int i = 0; i < H; i += 4) {
+        float2 e0, e1;
+        if (C::kInit) {   // the accumulator already holds s - LSE/scale
+          e0 = fmul2(make_float2(p[i], p[i + 1]), sl2_2);
+          e1 = fmul2(make_float2(p[i + 2], p[i + 3]), sl2_2);
+        } else {
 #ifdef SKR_EXP_NO_LDS   // timing experiment only (wrong results): LSE / D loads removed
-        const float4 l4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
+          const float4 l4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
 #else
-        const float4 l4 = ld_shared_f4(a_lse + i * 4);     // -lse2 is folded: p * sl2 - lse2
+          const float4 l4 = ld_shared_f4(a_lse + i * 4);     // -lse2 is folded: p * sl2 - lse2
 #endif
-        const float2 e0 = ffma2(make_float2(p[i], p[i + 1]), sl2_2, make_float2(-l4.x, -l4.y));
-        const float2 e1 = ffma2(make_float2(p[i + 2], p[i + 3]), sl2_2, make_float2(-l4.z, -l4.w));
+          e0 = ffma2(make_float2(p[i], p[i + 1]), sl2_2, make_float2(-l4.x, -l4.y));
+          e1 = ffma2(make_float2(p[i + 2], p[i + 3]), sl2_2, make_float2(-l4.z, -l4.w));
+        }
         // element (i % 8) < kPolyPer8 on the FMA pipe, the rest on MUFU
         p[i + 0] = (i % 8) + 0 < kPolyPer8 ? ex2_poly(e0.x) : ex2(e0.x);
         p[i + 1] = (i % 8) + 1 < kPolyPer8 ? ex2_poly(e0.y) : ex2(e0.y);
@@ -427,15 +485,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const int c = cb + 32 * b;
+              float2 t0 = make_float2(__uint_as_float(r[b][i]), __uint_as_float(r[b][i + 1]));
+              float2 t1 = make_float2(__uint_as_float(r[b][i + 2]), __uint_as_float(r[b][i + 3]));
+              if (!C::kInit) {   // kInit: the accumulator already holds dP - D
 #ifdef SKR_EXP_NO_LDS
-              const float4 d4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
+                const float4 d4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
 #else
-              const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
+                const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
 #endif
-              const float2 t0 = fadd2(make_float2(__uint_as_float(r[b][i]), __uint_as_float(r[b][i + 1])),
-                                      make_float2(-d4.x, -d4.y));
-              const float2 t1 = fadd2(make_float2(__uint_as_float(r[b][i + 2]), __uint_as_float(r[b][i + 3])),
-                                      make_float2(-d4.z, -d4.w));
+                t0 = fadd2(t0, make_float2(-d4.x, -d4.y));
+                t1 = fadd2(t1, make_float2(-d4.z, -d4.w));
+              }
               const float2 s0 = fmul2(make_float2(p[c + i], p[c + i + 1]), t0);
               const float2 s1 = fmul2(make_float2(p[c + i + 2], p[c + i + 3]), t1);
               p[c + i + 0] = s0.x, p[c + i + 1] = s0.y, p[c + i + 2] = s1.x, p[c + i + 3] = s1.y;
