@@ -764,8 +764,9 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
       const int v = e ? atoi(e) : -1;
       return (v >= 0 && v <= 4) ? v : -1;
     }();
-    // measured (profiles/bwd_period.py, S = 16K): no gain at d=64, a loss at d=128 -> MUFU only
-    const int pp = poly >= 0 ? poly : 0;
+    // measured (C2 / C5n1 bench sweeps): d=64 best at 1/8 once the LSE/D loads left the exp phase
+    // (it is then MUFU-bound), a loss at d=128 -> MUFU only
+    const int pp = poly >= 0 ? poly : (d == 64 ? 1 : 0);
     auto launch = [&](auto kern, int smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       kern<<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv, accumulate, dq_acc);
