@@ -14,8 +14,10 @@ Metric (BASELINE.json): useful causal attention TFLOP/s fwd+bwd = sum_seq 14*d*H
 divided by the step time (max over ranks), whole-job aggregate. Inputs (Q, K, V, dO of the batch
 plus activations) exceed the 126 MB L2, so no explicit flush is done between steps.
 
-Rank 0 prints ONE JSON line. Under torchrun (N>1) every rank is one CP rank of a single CP group
-(DP = 1) and the workload is weak-scaled: N x the N=1 batch, C per rank fixed.
+Rank 0 prints ONE JSON line. Under torchrun (N>1) the ranks form a DP x CP grid (--dp, default 1:
+one CP group of N ranks; row f4): CP groups are blocks of N/dp consecutive ranks, GDS/LPT bins the
+batch over the DP ranks and DACP places inside each CP group. The workload is weak-scaled: N x the
+N=1 batch, C per rank fixed.
 """
 from __future__ import annotations
 
@@ -45,6 +47,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="workload (default: C2, weak-scaled by N)")
+    ap.add_argument("--dp", type=int, default=1, help="DP degree of the DP x CP grid (CP = N / dp)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -58,15 +61,17 @@ def workload(args, world):
     name = args.config or "C2"
     cfg = CONFIGS[name]
     if name == "C2":
-        # weak scaling of configs[1]: N x (63 long-tail + one 32K) sequences, one CP group of N.
-        # For N >= 2 the BucketSize is set below the longest sequence (R33) so DACP shards it.
+        # weak scaling of configs[1]: N x (63 long-tail + one 32K) sequences over the DP x CP grid.
+        # With CP >= 2 the BucketSize is set below the longest sequence (R33) so DACP shards it.
+        cp = world // args.dp
         lens = np.concatenate([cfg.lengths(args.seed + r) for r in range(world)])
-        bucket = cfg.bucket if world == 1 else 24576
+        bucket = cfg.bucket if cp == 1 else 24576
+        return name, cfg, np.asarray(lens, np.int64), cfg.shape, cp, bucket
     else:
         lens = cfg.lengths(args.seed)
         bucket = cfg.bucket
-        if cfg.cp != world:
-            raise SystemExit(f"config {name} is for CP={cfg.cp}, launched with {world} ranks")
+        if cfg.cp * args.dp != world:
+            raise SystemExit(f"config {name} is for CP={cfg.cp} x DP={args.dp}, launched with {world} ranks")
     return name, cfg, np.asarray(lens, np.int64), cfg.shape, world, bucket
 
 
@@ -224,28 +229,32 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2505_19609_b200 import skrull as sk
-    from paper_2505_19609_b200.runtime import RankStep
+    from paper_2505_19609_b200.runtime import RankStep, dp_micro_batches, grid_coords
 
+    dp = args.dp
+    dp_rank, cp_rank, _ = grid_coords(rank, world, dp)
     name, cfg, lens, shp, cp, bucket = workload(args, world)
     shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
     h, hkv = shp.hidden, shp.kv_hidden
 
     # ---- a1-a4: host plan (every rank computes the identical plan)
     t0 = time.perf_counter()
-    plan = sk.skr_plan(lens, bucket, cp, 1, h, hkv)
+    plan = sk.skr_plan(lens, bucket, cp, dp, h, hkv)
     plan_us = (time.perf_counter() - t0) * 1e6
-    n_mb = int(plan["n_mb_per_dp"][0])
-    mbs = []
-    for j in range(n_mb):
-        idx = np.nonzero(plan["mb_of_seq"] == j)[0]
-        mbs.append((lens[idx], plan["assign"][idx]))
+    all_mbs = [[(ml, ma) for _, ml, ma in dp_micro_batches(plan, lens, d)] for d in range(dp)]
+    mbs = all_mbs[dp_rank]
+    n_mb = len(mbs)
 
-    comm = sk.Comm(world, rank) if world > 1 else None
+    comm = None
+    if cp > 1:
+        # one NCCL communicator per CP group (every rank takes part in creating every group)
+        groups = [dist.new_group(list(range(d * cp, (d + 1) * cp))) for d in range(dp)]
+        comm = sk.Comm(cp, cp_rank, group=groups[dp_rank], src=dp_rank * cp)
     side = torch.cuda.Stream(priority=-1)
     steps = []
     g = torch.Generator(device="cuda")
     for j, (ml, ma) in enumerate(mbs):
-        rs = RankStep(shape, ml, ma, cp, rank)
+        rs = RankStep(shape, ml, ma, cp, cp_rank)
         g.manual_seed(args.seed * 1_000_003 + rank * 1009 + j)
         R = max(rs.rows, 1)
         src = {k: torch.randn(R, hh, shp.d, device="cuda", generator=g).to(torch.bfloat16)
@@ -342,7 +351,7 @@ def run_ours(args):
         peaks, which = measured_peaks()
         # dominant kernel: forward or backward attention call of the local class at N=1
         # (algorithmic flops of this rank: 4 / 10 * d * Hq per causal pair it computes)
-        my_pairs = sum(rank_pairs(ml, ma, cp, rank) for ml, ma in mbs)
+        my_pairs = sum(rank_pairs(ml, ma, cp, cp_rank) for ml, ma in mbs)
         fwd_fl, bwd_fl = 4 * shp.d * shp.hq * my_pairs, 10 * shp.d * shp.hq * my_pairs
         dom = ("bwd", bwd_fl, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", fwd_fl, fwd_ms)
         achieved = dom[1] / (dom[2] * 1e-3) / 1e12
@@ -355,19 +364,25 @@ def run_ours(args):
             cpu = {"value": v, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"{n} shortest sequences ({toks} tokens) of the batch, fp64 numpy fwd+bwd, {t:.1f} s"}
         mean_rank = float(allv[:, 0].mean())
-        plan_pairs = [[rank_pairs(ml, ma, cp, r) for r in range(cp)] for ml, ma in mbs]
-        floor = sum(max(p) for p in plan_pairs) / max(1e-9, sum(sum(p) / cp for p in plan_pairs))
+        # plan floor (Eq. 8 style): per DP rank, sum over its micro-batches of the slowest CP rank's
+        # causal pairs; the slowest DP rank over the mean pairs per GPU
+        t_dp, tot = [], 0
+        for d_mbs in all_mbs:
+            pp = [[rank_pairs(ml, ma, cp, r) for r in range(cp)] for ml, ma in d_mbs]
+            t_dp.append(sum(max(p) for p in pp))
+            tot += sum(sum(p) for p in pp)
+        floor = max(t_dp) / max(1e-9, tot / world)
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": name, "desc": cfg.note,
                        "shape": f"Hq={shp.hq} Hkv={shp.hkv} d={shp.d}", "global_batch": int(len(lens)),
-                       "tokens": int(lens.sum()), "max_seq_len": int(lens.max()), "cp": cp, "dp": 1,
+                       "tokens": int(lens.sum()), "max_seq_len": int(lens.max()), "cp": cp, "dp": dp,
                        "bucket_tokens": int(bucket), "micro_batches": n_mb,
                        "distributed_seqs": int((plan["assign"] == -1).sum()),
                        "rollbacks": int(plan["n_rollbacks"]),
-                       "l2": "inputs larger than L2 (no flush)", "parallelism": f"cp{cp}"},
+                       "l2": "inputs larger than L2 (no flush)", "parallelism": f"dp{dp}xcp{cp}" if dp > 1 else f"cp{cp}"},
             "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]}", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic[0] if traffic else None,

@@ -235,3 +235,23 @@ def gather_rank_natural(per_seq, lens, assign, cp, rank, key):
     if not parts:
         return np.zeros((0,) + per_seq[0][key].shape[1:], np.float32)
     return np.concatenate(parts, axis=0)
+
+
+def grid_coords(rank: int, world: int, dp: int):
+    """DP x CP grid: rank -> (dp_rank, cp_rank, cp). CP groups are blocks of
+    cp consecutive ranks (one NVSwitch domain), DP ranks stride over them; GDS / LPT bins are per DP
+    rank (Alg. 2 line 1) and DACP places inside each CP group (Alg. 1)."""
+    if dp < 1 or world % dp:
+        raise ValueError(f"world {world} is not a multiple of dp {dp}")
+    cp = world // dp
+    return rank // cp, rank % cp, cp
+
+
+def dp_micro_batches(plan, lens, dp_rank: int):
+    """Micro-batches of one DP rank from skr_plan's output, in order: list of (seq indices, lens, assign)."""
+    lens = np.asarray(lens)
+    out = []
+    for j in range(int(plan["n_mb_per_dp"][dp_rank])):
+        idx = np.nonzero((plan["dp_of_seq"] == dp_rank) & (plan["mb_of_seq"] == j))[0]
+        out.append((idx, lens[idx], plan["assign"][idx]))
+    return out

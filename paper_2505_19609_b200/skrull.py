@@ -427,7 +427,9 @@ def skr_cast_f32_bf16(src, dst, stream=None):
 class Comm:
     """skr_comm wrapper; the NCCL unique id is broadcast over an existing torch process group."""
 
-    def __init__(self, nranks, rank, group=None):
+    def __init__(self, nranks, rank, group=None, src=0):
+        """nranks / rank: the CP group's size and this rank's index in it; `group` the torch process
+        group spanning it and `src` the GLOBAL rank of its first member (which draws the NCCL id)."""
         import torch
         import torch.distributed as dist
         n = _sig("skr_nccl_id_bytes", i32)()
@@ -439,7 +441,7 @@ class Comm:
             # an NCCL process group only moves device tensors; gloo takes host tensors
             if dist.get_backend(group) == "nccl":
                 t = t.cuda()
-            dist.broadcast(t, src=0, group=group)
+            dist.broadcast(t, src=src, group=group)
             t = t.cpu()
         buf = (C.c_uint8 * n)(*t.tolist())
         self.h = vp()

@@ -31,25 +31,27 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, C, q):
+def _worker(rank, world_size, port, C, q, dp=1):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dist.init_process_group("gloo", rank=rank, world_size=world_size)
         from paper_2505_19609_b200 import skrull as sk
-        from paper_2505_19609_b200.runtime import rank_natural_rows
+        from paper_2505_19609_b200.runtime import dp_micro_batches, grid_coords, rank_natural_rows
         hq, hkv, d = SHAPE
         lens = np.asarray(LENS, np.int64)
-        p = sk.skr_plan(lens, C, world, 1, hq * d, hkv * d)
+        # DP x CP grid (row f4): this rank's CP group = `world` consecutive ranks
+        dp_rank, rank, world = grid_coords(rank, world_size, dp)
+        groups = [dist.new_group(list(range(g * world, (g + 1) * world))) for g in range(dp)]
+        grp = groups[dp_rank]
+        p = sk.skr_plan(lens, C, world, dp, hq * d, hkv * d)
         # identical plans on every rank
-        mine = torch.tensor(np.concatenate([p["assign"], p["mb_of_seq"]]), dtype=torch.int64)
-        allp = [torch.zeros_like(mine) for _ in range(world)]
+        mine = torch.tensor(np.concatenate([p["assign"], p["mb_of_seq"], p["dp_of_seq"]]), dtype=torch.int64)
+        allp = [torch.zeros_like(mine) for _ in range(world_size)]
         dist.all_gather(allp, mine)
         assert all(torch.equal(x, mine) for x in allp)
         n_dist_total = 0
-        for j in range(int(p["n_mb_per_dp"][0])):
-            idx = np.nonzero(p["mb_of_seq"] == j)[0]
-            ml, ma = lens[idx], p["assign"][idx]
+        for idx, ml, ma in dp_micro_batches(p, lens, dp_rank):
             pr = sk.skr_pack_rank(ml, ma, world, rank)
             if pr["natural_rows"] == 0:
                 continue
@@ -64,7 +66,7 @@ def _worker(rank, world, port, C, q):
             n = min(P, len(packed))
             send[:n] = packed[:n]
             gathered = [torch.zeros(P, dtype=torch.int64) for _ in range(world)]
-            dist.all_gather(gathered, torch.from_numpy(send))
+            dist.all_gather(gathered, torch.from_numpy(send), group=grp)
             g = torch.cat(gathered).numpy()
             natural = np.full(pr["natural_rows"], -2, np.int64)
             for seq, c, owner, grow, nrow, ln in table:
@@ -78,7 +80,7 @@ def _worker(rank, world, port, C, q):
             for seq, c, owner, grow, nrow, ln in table:
                 rm[grow:grow + ln] = partial[nrow:nrow + ln]
             out = torch.zeros(P, dtype=torch.float64)
-            dist.reduce_scatter(out, list(torch.from_numpy(rm).chunk(world)))
+            dist.reduce_scatter(out, list(torch.from_numpy(rm).chunk(world)), group=grp)
             tot = sum(r + 1 for r in range(world))
             dr = pr["dist_rows"]
             assert np.array_equal(out.numpy()[:dr], tot * packed[:dr].astype(np.float64)), \
@@ -92,13 +94,14 @@ def _worker(rank, world, port, C, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,C", [(2, 1800), (3, 1300)])
-def test_cp_exchange_tables_over_gloo(world, C):
+@pytest.mark.parametrize("world,C,dp", [(2, 1800, 1), (3, 1300, 1), (4, 1100, 2)])
+def test_cp_exchange_tables_over_gloo(world, C, dp):
+    # (4, 1100, 2): a DP=2 x CP=2 grid, the exchange inside each CP group's sub-communicator
     pytest.importorskip("paper_2505_19609_b200.skrull")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, C, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, C, q, dp)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=240) for _ in range(world)]

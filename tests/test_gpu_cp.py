@@ -14,13 +14,14 @@ from oracle.cost_model import Model  # noqa: E402
 from tests.attn_harness import make_inputs, tol_ok  # noqa: E402
 
 
-def _run(lens, hq, hkv, d, N, C, bf16, seed):
+def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1):
     from paper_2505_19609_b200 import skrull as sk
-    from paper_2505_19609_b200.runtime import RankStep, gather_rank_natural, loopback_step
+    from paper_2505_19609_b200.runtime import RankStep, dp_micro_batches, gather_rank_natural, loopback_step
     shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16 if bf16 else sk.SKR_FP32)
-    p = sk.skr_plan(lens, C, N, 1, hq * d, hkv * d)
-    ref = oracle_plan(list(lens), C, N, 1, Model(hq * d, hkv * d))
+    p = sk.skr_plan(lens, C, N, dp, hq * d, hkv * d)
+    ref = oracle_plan(list(lens), C, N, dp, Model(hq * d, hkv * d))
     assert list(p["assign"]) == ref.assign                       # bit-exact plan
+    assert list(p["dp_of_seq"]) == ref.dp_of_seq and list(p["mb_of_seq"]) == ref.mb_of_seq
     inputs = make_inputs(lens, hq, hkv, d, seed=seed, bf16=bf16)
     tdt = torch.bfloat16 if bf16 else torch.float32
     src_key = {"o": "q", "dq": "q", "dk": "k", "dv": "k"}
@@ -28,9 +29,7 @@ def _run(lens, hq, hkv, d, N, C, bf16, seed):
             for k in ("o", "dq", "dk", "dv")}
     lse = [np.full((hq, int(S)), np.nan) for S in lens]
     n_dist = 0
-    for j in range(int(p["n_mb_per_dp"][0])):
-        idx = np.nonzero(p["mb_of_seq"] == j)[0]
-        ml, ma = np.asarray(lens)[idx], p["assign"][idx]
+    for idx, ml, ma in [mb for dr in range(dp) for mb in dp_micro_batches(p, lens, dr)]:
         n_dist += int((ma == -1).sum())
         mb_inputs = [inputs[i] for i in idx]
         ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
@@ -91,3 +90,11 @@ def test_n1_all_local():
     lens = [1, 17, 300, 129, 1024]
     n_dist, p = _run(lens, 14, 2, 64, 1, 4096, True, 4)
     assert n_dist == 0
+
+
+def test_dp2_x_cp2_grid():
+    # row f4: DP x CP grid (GDS/LPT bins over 2 DP ranks, DACP inside each CP group of 2); every DP
+    # rank's micro-batches run through its own CP group (loopback), all sequences covered once
+    lens = [1500, 37, 300, 129, 1, 600, 64, 2000, 250, 900, 17, 1100]
+    n_dist, p = _run(lens, 8, 2, 128, 2, 1200, True, 5, dp=2)
+    assert set(p["dp_of_seq"]) == {0, 1} and n_dist >= 1
