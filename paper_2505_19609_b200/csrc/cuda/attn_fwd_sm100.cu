@@ -2,12 +2,16 @@
 //
 // Work unit (CTA): one 128-row query tile of one segment x two q-heads of the same KV group
 // (GQA, R30), so each K/V tile is loaded once into shared memory and feeds both heads.
-// Warp roles (320 threads):
-//   warps 0-3  softmax warpgroup A (head ha), thread t owns query row t of the tile
-//   warps 4-7  softmax warpgroup B (head hb = ha + 1, if it exists in the group)
-//   warp 8     TMA producer: Q tiles once, then a ring of K/V tiles (SW128, 64-col boxes)
-//   warp 9     MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM; S(j+1) is issued as
+// Warp roles (576 threads):
+//   warps 0-7  softmax of head A (ha): two warpgroups split the 128 key columns of each S tile
+//              (warpgroup 0 keys [0,64), warpgroup 1 keys [64,128)); thread = query row of the tile,
+//              the two halves of a row combine their maxima through shared memory once per tile
+//   warps 8-15 softmax of head B (hb = ha + 1, if it exists in the group), same split
+//   warp 16    TMA producer: Q tiles once, then a ring of K/V tiles (SW128, 64-col boxes)
+//   warp 17    MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM; S(j+1) is issued as
 //              soon as the softmax has read S(j) (s_free), overlapping the exponentials of tile j
+// Two warpgroups per head halve the per-head softmax chain (S(j) -> exps -> P(j) -> PV(j) -> S(j+1)
+// is serial per head when P aliases S) and put four softmax warps on every sub-partition.
 // TMEM (512 cols): see Cfg.
 // Softmax: S row read with tcgen05.ld (no shuffles: one thread = one row), exp2 with the scale
 // folded in, running max kept in log2 units and O rescaled in TMEM only when the max grows by
@@ -72,7 +76,9 @@ __device__ __forceinline__ void trace_smw(int, int) {}
 #endif
 
 constexpr int BM = 128, BN = 128;
-constexpr int kThreads = 320;
+constexpr int kThreads = 576;
+constexpr int kSoftmax = 256;                // threads per head (two warpgroups)
+constexpr int kTmaWarp = 16, kMmaWarp = 17;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 template <int D>
@@ -83,7 +89,8 @@ struct Cfg {
   static constexpr int kUnits = D == 128 ? 4 : 6;        // K/V ring depth (units of one tile), <= 8
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQBytes;
-  static constexpr int kOffBar = kOffKV + kUnits * kKVBytes;
+  static constexpr int kOffRed = kOffKV + kUnits * kKVBytes;   // [head][tile parity][half][row] row maxima
+  static constexpr int kOffBar = kOffRed + 2 * 2 * 2 * BM * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;    // + barriers + alignment slack
   // TMEM columns. P (bf16 pairs) is the A operand of O += P V straight from TMEM (no smem traffic).
   // d = 64 : S_A[0,128) S_B[128,256) O_A[256,320) O_B[320,384) P_A[384,448) P_B[448,512)
@@ -102,7 +109,7 @@ struct Bars {  // kUnits <= 8
 };
 
 template <int D, int kPolyPer8>   // kPolyPer8: exponentials per 8 computed by ex2_poly on the FMA pipe
-__global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (16K regs) -> <= 168 regs
+__global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers per thread
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, int pairs_per_group) {
@@ -133,20 +140,20 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
     for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars->s_full[s], 1);
-      mbar_init(&bars->s_free[s], 128);
-      mbar_init(&bars->p_full[s], 128);
+      mbar_init(&bars->s_free[s], kSoftmax);
+      mbar_init(&bars->p_full[s], kSoftmax);
       mbar_init(&bars->pv_done[s], 1);
     }
     fence_mbar_init();
   }
   trace_init();
-  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  if (warp == kMmaWarp) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     // ================= TMA producer (warp-converged loop, one elected lane issues)
     if (elect_one()) {
       tma_prefetch_desc(&tm_q);
@@ -181,8 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
       }
     }
     pa.mark(1);
-    if (lane == 0) pa.flush(g_trace_smem, 8);
-  } else if (warp == 9) {
+    if (lane == 0) pa.flush(g_trace_smem, kTmaWarp);
+  } else if (warp == kMmaWarp) {
     // ================= MMA issuer: ONE elected thread runs the whole loop. Measured (profiles/
     // umma_probe.py): the tensor pipe buffers only about one MMA ahead of the issuing thread, and
     // re-entering an elected region per MMA group costs ~200 cycles (R2UR of the descriptors,
@@ -288,83 +295,81 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
         }
       }
       pa.mark(3);
-      pa.flush(g_trace_smem, 9);
+      pa.flush(g_trace_smem, kMmaWarp);
     }
     __syncwarp();
   } else {
-    // ================= softmax warpgroups
-    const int s = warp / 4;                 // 0 -> head A, 1 -> head B
+    // ================= softmax: head s = warp / 8, key-column half hf = (warp / 4) % 2
+    const int s = warp / 8, hf = (warp / 4) % 2;
     const int h = s == 0 ? ha : hb;
     if (h >= 0) {
+      constexpr int HN = BN / 2;               // key columns of this half
       const int row = (warp % 4) * 32 + lane;  // TMEM lane == query row of the tile
       const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
-      const uint32_t tS = tmem + lane_base + C::tS(s);
-      const uint32_t tO = tmem + lane_base + C::tO(s);
-      const uint32_t tP = tmem + lane_base + C::tP(s);
+      const uint32_t tS = tmem + lane_base + C::tS(s) + hf * HN;
+      const uint32_t tO = tmem + lane_base + C::tO(s) + hf * (D / 2);   // this half rescales / stores O[:, hf]
+      const uint32_t tP = tmem + lane_base + C::tP(s) + hf * (HN / 2);
+      float* red = reinterpret_cast<float*>(smem + C::kOffRed) + s * (2 * 2 * BM);   // [parity][half][row]
       const int qp = qp0 + row;                // this row's query position
       const float sl2 = a.scale * 1.4426950408889634f;
       float m_ref = -INFINITY, l = 0.f;
-      // (a strict ping-pong of the two heads' exp phases through named barriers was measured slower:
-      // one warp alone drives the MUFU at ~70% of its rate, two overlapping warps at ~92%)
-      PhaseAcct pa;   // 0 wait S, 1 TMEM load S, 2 mask + max, 3 wait PV, 4 rescale + store P, 6 exps
+      PhaseAcct pa;   // 0 wait S, 1 TMEM load S, 2 mask + max + exchange, 3 wait PV, 4 rescale + store P, 6 exps
       pa.start();
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&bars->s_full[s], j & 1);
         pa.mark(0);
-        if (lane == 0) trace_smw(30 + 20 * s + 0, j | (warp % 4) << 6);
         tc_fence_after();
-        // all four 32-column loads in flight under one wait (a wait per load serialises ~4 TMEM
-        // round trips on the path to s_free and the exponentials)
-        float x[BN];
+        float x[HN];
         {
-          uint32_t r[BN / 32][32];
+          uint32_t r[HN / 32][32];
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + 32 * c, r[c]);
+          for (int c = 0; c < HN / 32; ++c) tmem_ld32(tS + 32 * c, r[c]);
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c)
+          for (int c = 0; c < HN / 32; ++c)
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[32 * c + i] = __uint_as_float(r[c][i]);
         }
         if (!C::kPAlias) {
           tc_fence_before();
           mbar_arrive(&bars->s_free[s]);      // S_s TMEM may now take S_s(j+1)
-          pa.mark(1);
-          if (lane == 0) trace_smw(30 + 20 * s + 1, j | (warp % 4) << 6);
         }
-        const int kv0 = j * BN;
-        if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
+        pa.mark(1);
+        const int kv0 = j * BN + hf * HN;
+        if (kv0 + HN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
 #pragma unroll
-          for (int i = 0; i < BN; ++i)
+          for (int i = 0; i < HN; ++i)
             if (kv0 + i > qp) x[i] = -INFINITY;
         }
-        // row max: 8 independent chains of three-input max (a single 128-long chain is latency-bound)
+        // half-row max: 8 independent chains of three-input max, then combine with the other half
         float mxs[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mxs[i] = x[i];
 #pragma unroll
-        for (int i = 8; i < BN; i += 16)
+        for (int i = 8; i < HN; i += 16)
 #pragma unroll
-          for (int t = 0; t < 8; ++t) mxs[t] = fmax3(mxs[t], x[i + t], i + 8 + t < BN ? x[i + 8 + t] : x[i + t]);
-        const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
-                               fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+          for (int t = 0; t < 8; ++t) mxs[t] = fmax3(mxs[t], x[i + t], i + 8 + t < HN ? x[i + 8 + t] : x[i + t]);
+        float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                         fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+        float* rj = red + (j & 1) * (2 * BM);
+        rj[hf * BM + row] = mx;
+        tc_fence_before();                    // (d = 128) this half's S loads precede the partner's P stores
+        named_bar_sync(1 + s, kSoftmax);
+        tc_fence_after();
+        mx = fmaxf(mx, rj[(1 - hf) * BM + row]);
         const float m_new = fmaxf(m_ref, mx * sl2);
         pa.mark(2);
-        // tcgen05.ld/st are warp-collective: the rescale decision is made per warp (every lane of
-        // the warp moves its reference max to its own m_new; alpha == 1 where nothing changed)
+        // tcgen05.ld/st are warp-collective: the rescale decision is made per warp; the two halves of
+        // a row see the same combined maximum, so their warps decide identically
         const bool rescale = __any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0;
         const float alpha = (rescale && j > 0) ? ex2(m_ref - m_new) : 1.f;
         if (rescale) m_ref = m_new;
-        // P = exp2(S * scale * log2e - m_ref) into registers (bf16 pairs) before waiting for PV(j-1),
-        // so the PV MMA has the whole exponential phase to complete.
         const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-        pa.mark(2);
-        // packed fp32x2 FFMA / FADD: two elements per instruction; 2 x float2 = 4 row-sum chains
         float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
-        uint32_t pk[BN / 2];
+        uint32_t pk[HN / 2];
 #pragma unroll
-        for (int c = 0; c < BN; c += 8) {
+        for (int c = 0; c < HN; c += 8) {
           float pv[8];
 #pragma unroll
           for (int i = 0; i < 8; i += 2) {
@@ -378,7 +383,6 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
         }
         const float ls[4] = {ls2[0].x, ls2[0].y, ls2[1].x, ls2[1].y};
-        if (lane == 0) trace_smw(30 + 20 * s + 2, j | (warp % 4) << 6);
         pa.mark(6);
         // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
         if (j > 0) {
@@ -386,10 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           tc_fence_after();
         }
         pa.mark(3);
-        if (lane == 0) trace_smw(30 + 20 * s + 3, j | (warp % 4) << 6);
         if (rescale && j > 0) {
 #pragma unroll
-          for (int c = 0; c < D; c += 16) {
+          for (int c = 0; c < D / 2; c += 16) {
             uint32_t r[16];
             tmem_ld16(tO + c, r);
             tmem_wait_ld();
@@ -403,28 +406,25 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           }
         }
         l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
-#pragma unroll
-        for (int c0 = 0; c0 < BN / 2; c0 += 32) {
-          uint32_t q[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) q[i] = pk[c0 + i];
-          tmem_st32(tP + c0, q);
-        }
+        tmem_st32(tP, pk);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
         pa.mark(4);
-        if (lane == 0) trace_smw(30 + 20 * s + 4, j | (warp % 4) << 6);
       }
       if (lane == 0) pa.flush(g_trace_smem, warp);
-      // ---- epilogue: O / l -> bf16, LSE
+      // ---- epilogue: combine the halves' row sums, O / l -> bf16 (this half's d columns), LSE
+      float* lr = red + (n_kv & 1) * (2 * BM);   // a parity slot no half reads any more
+      lr[hf * BM + row] = l;
+      named_bar_sync(1 + s, kSoftmax);
+      l += lr[(1 - hf) * BM + row];
       mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
       tc_fence_after();
       const float inv_l = 1.f / l;
       const bool store = row < n_valid;
-      __nv_bfloat16* orow = out + ((size_t)(r0 + row) * a.hq + h) * D;
+      __nv_bfloat16* orow = out + ((size_t)(r0 + row) * a.hq + h) * D + hf * (D / 2);
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
+      for (int c = 0; c < D / 2; c += 32) {
         uint32_t r[32];
         tmem_ld32(tO + c, r);
         tmem_wait_ld();
@@ -440,12 +440,12 @@ __global__ void __launch_bounds__(kThreads, 1)   // 10 warps: 3 share an SMSP (1
           }
         }
       }
-      if (store) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+      if (store && hf == 0) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
 }  // namespace fwd

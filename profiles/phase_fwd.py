@@ -3,8 +3,8 @@
 Needs the phase-accounting build (no per-event traces, so the warps are not perturbed):
     SKR_KERNEL_TRACE=phase python -m paper_2505_19609_b200.build   # -> libskrull_trace.so
     python profiles/phase_fwd.py [d] [S]
-Prints cycles per KV tile of every phase for warps 0-7 (softmax A: 0-3, B: 4-7), the TMA warp (8)
-and the MMA thread (9).
+Prints cycles per KV tile of every phase for warps 0-15 (softmax: head A 0-7, head B 8-15; warps
+w and w+4 split the key columns of the same rows), the TMA warp (16) and the MMA thread (17).
 """
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -27,14 +27,14 @@ for _ in range(3):
     sk.skr_attn_fwd(shape, fs, q, k, v, o, lse)
     torch.cuda.synchronize()
 sk._lib.skr_debug_fwd_trace(buf, 8192)
-a = np.array(buf[:80], dtype=np.int64).reshape(10, 8)
+a = np.array(buf[:144], dtype=np.int64).reshape(18, 8)
 n_kv = S // 128   # block (0, 0) runs the LPT-first (longest) q tile
-names = {"sm": ["wait S", "ld S", "max", "wait PV", "store P", "-", "exps"], 8: ["wait slot", "issue"],
-         9: ["wait K", "wait V", "wait S/P", "issue"]}
+names = {"sm": ["wait S", "ld S", "max+xchg", "wait PV", "store P", "-", "exps"], 16: ["wait slot", "issue"],
+         17: ["wait K", "wait V", "wait S/P", "issue"]}
 print(f"d={d} S={S}: cycles per KV tile (n_kv={n_kv})")
-for w in range(10):
-    lab = names["sm"] if w < 8 else names[w]
+for w in range(18):
+    lab = names["sm"] if w < 16 else names[w]
     row = "  ".join(f"{lab[i]} {a[w, i] / n_kv:7.0f}" for i in range(len(lab)))
     tot = a[w, :len(lab)].sum() / n_kv
-    who = f"{'A' if w < 4 else 'B'} w{w % 4}" if w < 8 else ("TMA" if w == 8 else "MMA")
+    who = f"{'A' if w < 8 else 'B'}{(w // 4) % 2} w{w % 4}" if w < 16 else ("TMA" if w == 16 else "MMA")
     print(f"{who:5s} total {tot:7.0f} | {row}")
