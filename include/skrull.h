@@ -197,6 +197,37 @@ skr_status skr_scatter_chunks(const void* natural, const int32_t* chunk_table, i
 /* a9 cast: fp32 -> bf16, n elements. */
 skr_status skr_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
 
+/* Row f3 (first step): the CP exchange over peer memory instead of NCCL collectives
+ * (P:122 names the all-gather / its mirror, P:57 leaves the CP method open).
+ * Buffers of the other ranks of the CP group are mapped with CUDA IPC; on NVLink / NVSwitch the
+ * kernels' loads and stores are peer accesses. All pointer arrays are DEVICE arrays of nranks
+ * uint64 device addresses (this rank's own buffer at index rank). */
+int32_t skr_ipc_blob_bytes(void); /* size of an export blob: IPC handle + offset in its allocation */
+/* Export a device pointer (may point inside a larger cudaMalloc allocation) for another process. */
+skr_status skr_ipc_export(const void* dev_ptr, void* blob_out);
+/* Map another process's exported pointer (one mapping per allocation per process, refcounted);
+ * SKR_E_CUDA if the handle cannot be opened (e.g. the same process that exported it). */
+skr_status skr_ipc_import(const void* blob, void** dev_ptr_out);
+skr_status skr_ipc_close_all(void); /* unmap every imported allocation */
+/* a6 as one pass: for each chunk-table row, len rows of row_bytes from
+ * peer_packed[owner] + (gathered_row - owner*pad_rows_P) rows  ->  natural + natural_row rows.
+ * Replaces all-gather + skr_gather_chunks (no [N][P] staging buffer). */
+skr_status skr_peer_gather_chunks(const uint64_t* peer_packed, const int32_t* chunk_table, int32_t n_chunks,
+                                  int32_t row_bytes, int32_t pad_rows_P, void* natural, void* stream);
+/* a9 as one pass: for each chunk OWNED by `rank`, dst row (gathered_row - rank*pad_rows_P + r) =
+ * sum over ranks 0..nranks-1 (fixed order) of peer_partials[rank'] fp32 row (natural_row + r),
+ * row_elems fp32 per row; dst bf16 (round to nearest even) if dst_bf16, else fp32.
+ * Replaces skr_scatter_chunks + reduce-scatter + skr_cast_f32_bf16. */
+skr_status skr_peer_reduce_chunks(const uint64_t* peer_partials, int32_t nranks, int32_t rank,
+                                  const int32_t* chunk_table, int32_t n_chunks, int32_t row_elems,
+                                  int32_t pad_rows_P, void* dst, int32_t dst_bf16, void* stream);
+/* Epoch flags (uint32 per rank): signal stores `epoch` into slot `rank` of every peer's flag array
+ * (system-scope release after a system fence, ordered after this stream's earlier work); wait
+ * blocks the stream until every slot of this rank's flags reached `epoch`, or sets *err = 1 after
+ * ~10 s (a peer never signalled) instead of hanging. */
+skr_status skr_peer_signal(const uint64_t* peer_flags, int32_t nranks, int32_t rank, uint32_t epoch, void* stream);
+skr_status skr_peer_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, int32_t* err, void* stream);
+
 /* CP communicator (rows a6/a9; NCCL inside the CP group over NVLink/NVSwitch). */
 typedef struct skr_comm skr_comm;
 int32_t skr_nccl_id_bytes(void); /* size of the unique id blob (128) */

@@ -181,6 +181,92 @@ class RankStep:
             main.wait_event(ev_rs)
 
 
+    # ------------------------------------------------------------------ row f3: peer-memory exchange
+    def connect_peer(self, peer):
+        """Collective over the CP group: map the peers' packed K/V and natural fp32 dK/dV partials."""
+        self.peer = peer
+        if self.has_dist:
+            self.peer_k, self.peer_v, self.peer_dk, self.peer_dv = peer.exchange(
+                [self.k, self.v, self.dk_nat, self.dv_nat])
+
+    def peer_gather(self, stream=None):
+        sk.skr_peer_gather_chunks(self.peer_k, self.chunks, self.n_chunks, self.P, self.k_nat, stream)
+        sk.skr_peer_gather_chunks(self.peer_v, self.chunks, self.n_chunks, self.P, self.v_nat, stream)
+
+    def peer_reduce(self, stream=None):
+        re = self.shape.hkv * self.shape.d
+        sk.skr_peer_reduce_chunks(self.peer_dk, self.cp, self.rank, self.chunks, self.n_chunks, re, self.P,
+                                  self.dk, stream)
+        sk.skr_peer_reduce_chunks(self.peer_dv, self.cp, self.rank, self.chunks, self.n_chunks, re, self.P,
+                                  self.dv, stream)
+
+    def forward_peer(self, q_src, k_src, v_src, side):
+        """Eq. 2 with the a6 exchange as one peer-gather pass: pack; signal 'packed K/V ready'; on the
+        side stream wait for every peer, then copy each distributed chunk from its owner's packed
+        buffer into the natural buffer, while the main stream runs the local tiles."""
+        main = torch.cuda.current_stream()
+        self.pack_qkv(q_src, k_src, v_src)
+        if self.has_dist:
+            e = self.peer.signal(main)
+            with torch.cuda.stream(side):
+                self.peer.wait(e, side)
+                self.peer_gather(side)
+                ev_kv = torch.cuda.Event()
+                ev_kv.record(side)
+        self.fwd_local()
+        if self.has_dist:
+            main.wait_event(ev_kv)
+            self.fwd_dist()
+
+    def backward_peer(self, do_src, side):
+        """Mirror (R24): distributed tiles first; signal 'partials ready'; on the side stream wait,
+        sum every owned chunk over the peers' partials straight into the packed bf16 dK/dV prefix,
+        then a second epoch ('partials consumed') before the buffers may be reused."""
+        main = torch.cuda.current_stream()
+        self.pack_do(do_src)
+        if self.has_dist:
+            self.bwd_dist()
+            e = self.peer.signal(main)
+            with torch.cuda.stream(side):
+                self.peer.wait(e, side)
+                self.peer_reduce(side)
+                e2 = self.peer.signal(side)
+                self.peer.wait(e2, side)
+                ev_rs = torch.cuda.Event()
+                ev_rs.record(side)
+        self.bwd_local()
+        if self.has_dist:
+            main.wait_event(ev_rs)
+
+
+def loopback_peer_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
+    """Row f3 on ONE GPU in one process: the peer-gather / peer-reduce kernels with the other
+    emulated ranks' buffers as the 'peer' addresses (no flags needed: the ranks run in order)."""
+    N = len(ranks)
+    for r, x in enumerate(ranks):
+        x.pack_qkv(q_srcs[r], k_srcs[r], v_srcs[r])
+        x.pack_do(do_srcs[r])
+    if ranks[0].has_dist:
+        addr = lambda name: torch.tensor([getattr(y, name).data_ptr() for y in ranks], dtype=torch.int64,  # noqa: E731
+                                         device=ranks[0].dev)
+        for x in ranks:
+            x.peer_k, x.peer_v, x.peer_dk, x.peer_dv = addr("k"), addr("v"), addr("dk_nat"), addr("dv_nat")
+            x.peer_gather()
+    for x in ranks:
+        x.fwd_local()
+        if x.has_dist:
+            x.fwd_dist()
+    if ranks[0].has_dist:
+        for x in ranks:
+            x.bwd_dist()
+        for x in ranks:
+            x.peer_reduce()
+    for x in ranks:
+        x.bwd_local()
+    del N
+    return ranks
+
+
 def loopback_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
     """Debug aid: run N RankSteps of one micro-batch on ONE GPU, the all-gather and
     reduce-scatter replaced by device copies. Same kernels and tables as production."""

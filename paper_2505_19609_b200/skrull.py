@@ -423,6 +423,103 @@ def skr_cast_f32_bf16(src, dst, stream=None):
     _check(fn(_tptr(src), _tptr(dst), src.numel(), _stream(stream)))
 
 
+# ---------------------------------------------------------------------------- f3: peer-memory exchange
+def skr_ipc_blob_bytes() -> int:
+    return _sig("skr_ipc_blob_bytes", i32)()
+
+
+def skr_ipc_export(t) -> bytes:
+    """IPC blob (handle + offset) of a device tensor's storage start."""
+    n = skr_ipc_blob_bytes()
+    buf = (C.c_uint8 * n)()
+    _check(_sig("skr_ipc_export", i32, vp, vp)(_tptr(t), C.cast(buf, vp)))
+    return bytes(buf)
+
+
+def skr_ipc_import(blob: bytes) -> int:
+    """Device address in this process of another process's exported tensor."""
+    buf = (C.c_uint8 * len(blob))(*blob)
+    out = vp()
+    _check(_sig("skr_ipc_import", i32, vp, P(vp))(C.cast(buf, vp), C.byref(out)))
+    return int(out.value)
+
+
+def skr_ipc_close_all():
+    _check(_sig("skr_ipc_close_all", i32)())
+
+
+def skr_peer_gather_chunks(peer_packed, chunk_table, n_chunks, pad_rows_P, natural, stream=None):
+    """peer_packed: int64 device tensor [N] of the ranks' packed K (or V) buffer addresses."""
+    fn = _sig("skr_peer_gather_chunks", i32, vp, vp, i32, i32, i32, vp, vp)
+    rb = natural[0].numel() * natural.element_size()
+    _check(fn(_tptr(peer_packed), _tptr(chunk_table), int(n_chunks), rb, int(pad_rows_P), _tptr(natural),
+              _stream(stream)))
+
+
+def skr_peer_reduce_chunks(peer_partials, nranks, rank, chunk_table, n_chunks, row_elems, pad_rows_P, dst,
+                           stream=None):
+    """peer_partials: int64 device tensor [N] of the ranks' fp32 natural partial buffers; dst bf16 or fp32."""
+    import torch
+    fn = _sig("skr_peer_reduce_chunks", i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, vp)
+    _check(fn(_tptr(peer_partials), int(nranks), int(rank), _tptr(chunk_table), int(n_chunks), int(row_elems),
+              int(pad_rows_P), _tptr(dst), 1 if dst.dtype == torch.bfloat16 else 0, _stream(stream)))
+
+
+def skr_peer_signal(peer_flags, nranks, rank, epoch, stream=None):
+    _check(_sig("skr_peer_signal", i32, vp, i32, i32, C.c_uint32, vp)(_tptr(peer_flags), int(nranks), int(rank),
+                                                                      int(epoch) & 0xFFFFFFFF, _stream(stream)))
+
+
+def skr_peer_wait(flags, nranks, epoch, err, stream=None):
+    _check(_sig("skr_peer_wait", i32, vp, i32, C.c_uint32, vp, vp)(_tptr(flags), int(nranks), int(epoch) & 0xFFFFFFFF,
+                                                                   _tptr(err), _stream(stream)))
+
+
+class PeerComm:
+    """Row f3 exchange context of one CP group: the epoch-flag array every peer writes into, and the
+    IPC exchange of buffer addresses over a torch process group (control plane only)."""
+
+    MAX_RANKS = 64
+
+    def __init__(self, nranks, rank, group=None):
+        import torch
+        self.nranks, self.rank, self.group = nranks, rank, group
+        self.flags = torch.zeros(self.MAX_RANKS, dtype=torch.int32, device="cuda")
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.epoch = 0
+        torch.cuda.synchronize()
+        self.peer_flags = self.exchange([self.flags])[0]
+
+    def exchange(self, tensors):
+        """-> one int64 device tensor [nranks] of addresses per input tensor (collective)."""
+        import torch
+        import torch.distributed as dist
+        blobs = [skr_ipc_export(t) for t in tensors]
+        allb = [None] * self.nranks
+        dist.all_gather_object(allb, blobs, group=self.group)
+        out = []
+        for i, t in enumerate(tensors):
+            addrs = [t.data_ptr() if r == self.rank else skr_ipc_import(allb[r][i]) for r in range(self.nranks)]
+            out.append(torch.tensor(addrs, dtype=torch.int64, device="cuda"))
+        return out
+
+    def signal(self, stream=None) -> int:
+        """Enqueue: this rank reached the next epoch. Returns the epoch to wait for."""
+        self.epoch += 1
+        skr_peer_signal(self.peer_flags, self.nranks, self.rank, self.epoch, stream)
+        return self.epoch
+
+    def wait(self, epoch, stream=None):
+        skr_peer_wait(self.flags, self.nranks, epoch, self.err, stream)
+
+    def check(self):
+        if int(self.err.item()):
+            raise SkrullError(SKR_E_CUDA, "peer exchange: a peer never signalled (10 s)")
+
+    def close(self):
+        skr_ipc_close_all()
+
+
 # ---------------------------------------------------------------------------- CP communicator
 class Comm:
     """skr_comm wrapper; the NCCL unique id is broadcast over an existing torch process group."""

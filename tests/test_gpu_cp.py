@@ -14,9 +14,10 @@ from oracle.cost_model import Model  # noqa: E402
 from tests.attn_harness import make_inputs, tol_ok  # noqa: E402
 
 
-def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1):
+def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1, exchange="nccl"):
     from paper_2505_19609_b200 import skrull as sk
-    from paper_2505_19609_b200.runtime import RankStep, dp_micro_batches, gather_rank_natural, loopback_step
+    from paper_2505_19609_b200.runtime import (RankStep, dp_micro_batches, gather_rank_natural, loopback_peer_step,
+                                               loopback_step)
     shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16 if bf16 else sk.SKR_FP32)
     p = sk.skr_plan(lens, C, N, dp, hq * d, hkv * d)
     ref = oracle_plan(list(lens), C, N, dp, Model(hq * d, hkv * d))
@@ -35,7 +36,8 @@ def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1):
         ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
         srcs = {k: [torch.from_numpy(gather_rank_natural(mb_inputs, ml, ma, N, r, k)).to("cuda", tdt)
                     for r in range(N)] for k in ("q", "k", "v", "do")}
-        loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+        (loopback_peer_step if exchange == "peer" else loopback_step)(ranks, srcs["q"], srcs["k"], srcs["v"],
+                                                                       srcs["do"])
         torch.cuda.synchronize()
         for r, rs in enumerate(ranks):
             pr = rs.pr
@@ -98,3 +100,19 @@ def test_dp2_x_cp2_grid():
     lens = [1500, 37, 300, 129, 1, 600, 64, 2000, 250, 900, 17, 1100]
     n_dist, p = _run(lens, 8, 2, 128, 2, 1200, True, 5, dp=2)
     assert set(p["dp_of_seq"]) == {0, 1} and n_dist >= 1
+
+
+@pytest.mark.parametrize("case", ["c1_fp32", "bf16_n2", "bf16_n4", "rollback_d64"])
+def test_peer_exchange_loopback(case):
+    # row f3: the a6 / a9 exchange as peer-gather / peer-reduce kernels (one pass each) instead of
+    # all-gather + reorder and permute + reduce-scatter + cast; same oracle bar
+    lens = [1500, 37, 300, 129, 1, 600, 64, 2000, 250]
+    if case == "c1_fp32":
+        n_dist, _ = _run([17, 33, 64, 90, 128, 200, 256, 300], 2, 2, 64, 2, 600, False, 0, exchange="peer")
+    elif case == "bf16_n2":
+        n_dist, _ = _run(lens, 8, 2, 128, 2, 1600, True, 2, exchange="peer")
+    elif case == "bf16_n4":
+        n_dist, _ = _run(lens, 8, 2, 128, 4, 900, True, 2, exchange="peer")
+    else:
+        n_dist, _ = _run([3, 5, 2, 700, 800, 1, 7], 14, 2, 64, 4, 400, True, 3, exchange="peer")
+    assert n_dist >= 1
