@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="workload (default: C2, weak-scaled by N)")
     ap.add_argument("--dp", type=int, default=1, help="DP degree of the DP x CP grid (CP = N / dp)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="CP exchange: NCCL all-gather / reduce-scatter, or the peer-memory kernels (row f3)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -225,9 +227,16 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # SKR_BENCH_BACKEND=gloo: control plane over gloo with every rank on the visible GPUs modulo
+    # their count -- a functional multi-rank run on ONE GPU for --exchange peer (timings meaningless)
+    backend = os.environ.get("SKR_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2505_19609_b200 import skrull as sk
     from paper_2505_19609_b200.runtime import RankStep, dp_micro_batches, grid_coords
 
@@ -247,24 +256,36 @@ def run_ours(args):
 
     comm = None
     if cp > 1:
-        # one NCCL communicator per CP group (every rank takes part in creating every group)
+        # one communicator per CP group (every rank takes part in creating every group)
         groups = [dist.new_group(list(range(d * cp, (d + 1) * cp))) for d in range(dp)]
-        comm = sk.Comm(cp, cp_rank, group=groups[dp_rank], src=dp_rank * cp)
+        if args.exchange == "peer":
+            comm = sk.PeerComm(cp, cp_rank, group=groups[dp_rank])
+        else:
+            comm = sk.Comm(cp, cp_rank, group=groups[dp_rank], src=dp_rank * cp)
     side = torch.cuda.Stream(priority=-1)
     steps = []
     g = torch.Generator(device="cuda")
     for j, (ml, ma) in enumerate(mbs):
         rs = RankStep(shape, ml, ma, cp, cp_rank)
+        if args.exchange == "peer" and comm is not None:
+            rs.connect_peer(comm)              # collective inside the CP group
         g.manual_seed(args.seed * 1_000_003 + rank * 1009 + j)
         R = max(rs.rows, 1)
         src = {k: torch.randn(R, hh, shp.d, device="cuda", generator=g).to(torch.bfloat16)
                for k, hh in (("q", shp.hq), ("k", shp.hkv), ("v", shp.hkv), ("do", shp.hq))}
         steps.append((rs, src))
 
-    def one_step():
-        for rs, src in steps:
+    def fwd_bwd(rs, src):
+        if args.exchange == "peer" and comm is not None:
+            rs.forward_peer(src["q"], src["k"], src["v"], side)
+            rs.backward_peer(src["do"], side)
+        else:
             rs.forward(src["q"], src["k"], src["v"], comm, side)
             rs.backward(src["do"], comm, side)
+
+    def one_step():
+        for rs, src in steps:
+            fwd_bwd(rs, src)
 
     def barrier():
         if world > 1:
@@ -317,8 +338,7 @@ def run_ours(args):
             for (rs, src), hs, o in zip(steps, host, outs):
                 for k in src:
                     src[k].copy_(hs[k], non_blocking=True)
-                rs.forward(src["q"], src["k"], src["v"], comm, side)
-                rs.backward(src["do"], comm, side)
+                fwd_bwd(rs, src)
                 for k in o:
                     o[k].copy_(getattr(rs, k)[:rs.rows], non_blocking=True)
 
@@ -338,6 +358,8 @@ def run_ours(args):
     # ---- reduce over ranks: max (headline), per-rank list (imbalance)
     vals = torch.tensor([my_ms, fwd_ms, bwd_ms, e2e[0] if e2e else 0.0], device="cuda", dtype=torch.float64)
     if world > 1:
+        if backend != "nccl":
+            vals = vals.cpu()                 # gloo moves host tensors
         allv = [torch.zeros_like(vals) for _ in range(world)]
         dist.all_gather(allv, vals)
         allv = torch.stack(allv).cpu().numpy()
@@ -357,7 +379,7 @@ def run_ours(args):
         achieved = dom[1] / (dom[2] * 1e-3) / 1e12
         traffic = ncu_traffic(name, world, dom[0])
         peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-        gpu_launches = args.steps * sum(rs.launches_per_step() for rs, _ in steps)
+        gpu_launches = args.steps * sum(rs.launches_per_step(args.exchange) for rs, _ in steps)
         cpu = None
         if not args.no_cpu_baseline:
             v, n, toks, t = cpu_oracle_sample(lens, shp, args.cpu_seconds, args.seed)
@@ -376,13 +398,14 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": name, "desc": cfg.note,
+            "config": {"workload": name, "desc": cfg.note if world == 1 else f"{cfg.note}; weak-scaled x{world}",
                        "shape": f"Hq={shp.hq} Hkv={shp.hkv} d={shp.d}", "global_batch": int(len(lens)),
                        "tokens": int(lens.sum()), "max_seq_len": int(lens.max()), "cp": cp, "dp": dp,
                        "bucket_tokens": int(bucket), "micro_batches": n_mb,
                        "distributed_seqs": int((plan["assign"] == -1).sum()),
                        "rollbacks": int(plan["n_rollbacks"]),
-                       "l2": "inputs larger than L2 (no flush)", "parallelism": f"dp{dp}xcp{cp}" if dp > 1 else f"cp{cp}"},
+                       "l2": "inputs larger than L2 (no flush)", "parallelism": f"dp{dp}xcp{cp}" if dp > 1 else f"cp{cp}",
+                       "exchange": args.exchange if cp > 1 else None},
             "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]}", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic[0] if traffic else None,

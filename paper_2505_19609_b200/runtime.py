@@ -66,7 +66,7 @@ class RankStep:
             self.dk_rm, self.dv_rm = e(N * P, hkv, d, dt=f32), e(N * P, hkv, d, dt=f32)
             self.dk_red, self.dv_red = e(P, hkv, d, dt=f32), e(P, hkv, d, dt=f32)
 
-    def launches_per_step(self) -> int:
+    def launches_per_step(self, exchange="nccl") -> int:
         """Kernels of this library launched by one forward + backward of this micro-batch."""
         n = 0
         if self.rows:
@@ -75,9 +75,11 @@ class RankStep:
         n += (self.loc_f.n_tiles > 0) + (self.loc_b.n_tiles > 0) + 2 * (loc_rows > 0)
         if self.has_dist:
             dist_rows = self.dist_b.row_end - self.dist_b.row_begin
-            n += 2 + (self.dist_f.n_tiles > 0)                # reorder K, V; fwd
-            n += (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)
-            n += 2 + 2 * (self.dist_rows > 0)                 # scatter dK, dV; cast dK, dV
+            n += (self.dist_f.n_tiles > 0) + (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)
+            if exchange == "peer":
+                n += 2 + 2 + 3 * 2                            # gather K, V; reduce dK, dV; 3 signal+wait
+            else:
+                n += 2 + 2 + 2 * (self.dist_rows > 0)         # reorder K, V; scatter dK, dV; cast dK, dV
         return n
 
     # ------------------------------------------------------------------ phases
