@@ -381,7 +381,7 @@ def run_ours(args):
         peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
         gpu_launches = args.steps * sum(rs.launches_per_step(args.exchange) for rs, _ in steps)
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the oracle baseline is an N=1 figure
             v, n, toks, t = cpu_oracle_sample(lens, shp, args.cpu_seconds, args.seed)
             cpu = {"value": v, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"{n} shortest sequences ({toks} tokens) of the batch, fp64 numpy fwd+bwd, {t:.1f} s"}
