@@ -12,6 +12,20 @@
 
 namespace skr {
 
+// Blocks per chunk for the chunk-table kernels (grid.y = chunks): enough that the whole grid is
+// ~8 blocks per SM however few chunks there are (one 128K sequence over CP=2 has 4 chunks).
+int chunk_blocks_x(int n_chunks) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!sms) sms = 148;
+  }
+  const int y = std::max(1, std::min(n_chunks, 65535));
+  return std::max(1, std::min(4096, (sms * 8 + y - 1) / y));
+}
+
 static int grid_for(int64_t work_items, int threads) {
   static int sms = 0;
   if (!sms) {
@@ -101,7 +115,7 @@ SKR_EXPORT skr_status skr_gather_chunks(const void* gathered, const int32_t* chu
   if (n_chunks == 0) return SKR_OK;
   SKR_REQUIRE(gathered && chunk_table && natural, "skr_gather_chunks: null pointer");
   if (skr_status e = check_sm100()) return e;
-  dim3 grid(8, std::min(n_chunks, 65535));
+  dim3 grid(chunk_blocks_x(n_chunks), std::min(n_chunks, 65535));
   chunks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)gathered, chunk_table, n_chunks, row_bytes / 16,
                                                         (uint4*)natural, 1);
   return launch_status("gather_chunks");
@@ -121,7 +135,7 @@ SKR_EXPORT skr_status skr_scatter_chunks(const void* natural, const int32_t* chu
   if (cudaMemsetAsync(rankmajor, 0, (size_t)cp * pad_rows_P * row_bytes, st) != cudaSuccess)
     return fail(SKR_E_CUDA, "scatter memset");
   if (n_chunks == 0) return SKR_OK;
-  dim3 grid(8, std::min(n_chunks, 65535));
+  dim3 grid(chunk_blocks_x(n_chunks), std::min(n_chunks, 65535));
   chunks_kernel<<<grid, 256, 0, st>>>((const uint4*)natural, chunk_table, n_chunks, row_bytes / 16,
                                       (uint4*)rankmajor, 0);
   return launch_status("scatter_chunks");

@@ -25,6 +25,8 @@
 
 namespace skr {
 
+int chunk_blocks_x(int n_chunks);   // movement.cu
+
 // chunk table rows: {seq, chunk, owner, gathered_row, natural_row, len}
 __global__ void peer_gather_kernel(const uint64_t* __restrict__ peer_base, const int32_t* __restrict__ table,
                                    int n_chunks, int vpr, int pad_rows_P, uint4* __restrict__ natural) {
@@ -176,7 +178,7 @@ SKR_EXPORT skr_status skr_peer_gather_chunks(const uint64_t* peer_packed, const 
   if (n_chunks == 0) return SKR_OK;
   SKR_REQUIRE(peer_packed && chunk_table && natural, "skr_peer_gather_chunks: null pointer");
   if (skr_status e = check_sm100()) return e;
-  dim3 grid(8, std::min(n_chunks, 65535));
+  dim3 grid(chunk_blocks_x(n_chunks), std::min(n_chunks, 65535));
   peer_gather_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(peer_packed, chunk_table, n_chunks, row_bytes / 16,
                                                             pad_rows_P, (uint4*)natural);
   return launch_status("peer_gather_chunks");
@@ -191,7 +193,8 @@ SKR_EXPORT skr_status skr_peer_reduce_chunks(const uint64_t* peer_partials, int3
   if (n_chunks == 0) return SKR_OK;
   SKR_REQUIRE(peer_partials && chunk_table && dst, "skr_peer_reduce_chunks: null pointer");
   if (skr_status e = check_sm100()) return e;
-  dim3 grid(8, std::min(n_chunks, 65535));
+  // only the chunks this rank owns (about 1/nranks of them) do work: size the blocks per chunk for those
+  dim3 grid(chunk_blocks_x(std::max(1, n_chunks / nranks)), std::min(n_chunks, 65535));
   if (dst_bf16)
     peer_reduce_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(peer_partials, nranks, rank, chunk_table,
                                                                      n_chunks, row_elems / 4, pad_rows_P, dst);
