@@ -1,8 +1,10 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the same
 plan, RankStep tables and C-ABI calls), on outputs the fp64 oracle can compute one by one.
 
-Full batches are far beyond what the naive oracle finishes in seconds (C2's 32K sequence alone is
-~1e12 fp64 flop), so each check is on a SAMPLE whose oracle values are exact restrictions of the
+BASELINE configs[1..4] at full size: C2, C3n2 (configs[2]), C4 (configs[3], CP=8 loopback), C5n1
+(configs[4] at N=1). Full batches are far beyond what the naive oracle finishes in seconds (C2's
+32K sequence alone is ~1e12 fp64 flop), so each check is on a SAMPLE whose oracle values are exact
+restrictions of the
 plain definition:
   * query row i of sequence s: O_i, LSE_i and dQ_i depend only on q_i, do_i and keys 0..i
     -> oracle.attn_fwd / attn_bwd on the single row with q_pos = i;
@@ -100,7 +102,7 @@ def _check(name, got, ref, where):
     assert ok, f"{name} {where}: err {err} > {bound}"
 
 
-@pytest.mark.parametrize("cfg_name", ["C2", "C5n1", "C3n2"])
+@pytest.mark.parametrize("cfg_name", ["C2", "C5n1", "C3n2", "C4"])
 def test_fullsize_sampled(cfg_name):
     cfg, lens, runs, loc = _launch(cfg_name, 0)
     rng = np.random.default_rng(1234)
