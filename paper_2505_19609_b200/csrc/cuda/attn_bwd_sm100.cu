@@ -653,40 +653,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 13) tmem_dealloc<512>(tmem);
 }
 
-// D[h][r] = sum_c dO[r][h][c] * O[r][h][c] (bf16 in, fp32 out); zero the dQ accumulator rows.
+// D[h][r] = sum_c dO[r][h][c] * O[r][h][c] (bf16 in, fp32 out). A group of D/8 threads owns one
+// (row, head): 16-byte loads of O and dO, shuffle-reduced inside the group. (The dQ accumulator is
+// zeroed by a memset, which runs at copy bandwidth.)
 template <int D>
 __global__ void preprocess_kernel(int row_begin, int row_end, int hq, const __nv_bfloat16* __restrict__ o,
-                                  const __nv_bfloat16* __restrict__ dout, float* __restrict__ Dbuf, int ld,
-                                  float* __restrict__ dq_acc) {
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  const int64_t row = row_begin + gw / hq;
-  const int h = gw % hq;
-  if (row >= row_end) return;
-  const size_t base = ((size_t)row * hq + h) * D;
-  constexpr int E = D / 32;  // 2 or 4 elements per lane
+                                  const __nv_bfloat16* __restrict__ dout, float* __restrict__ Dbuf, int ld) {
+  constexpr int G = D / 8;                       // threads per (row, head): 8 or 16
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int sub = threadIdx.x % G;
+  const int64_t row = row_begin + gid / hq;
+  const int h = gid % hq;
+  const bool ok = row < row_end;
   float s = 0.f;
-  if (E == 4) {
-    const uint2 a = *reinterpret_cast<const uint2*>(o + base + lane * 4);
-    const uint2 b = *reinterpret_cast<const uint2*>(dout + base + lane * 4);
+  if (ok) {
+    const size_t base = ((size_t)row * hq + h) * D + sub * 8;
+    const uint4 a = *reinterpret_cast<const uint4*>(o + base);
+    const uint4 b = *reinterpret_cast<const uint4*>(dout + base);
     const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
     const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
-    for (int i = 0; i < 2; ++i) {
-      float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
-      s += x.x * y.x + x.y * y.y;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
+      s = fmaf(x.x, y.x, fmaf(x.y, y.y, s));
     }
-    *reinterpret_cast<float4*>(dq_acc + base + lane * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
-  } else {
-    const uint32_t a = *reinterpret_cast<const uint32_t*>(o + base + lane * 2);
-    const uint32_t b = *reinterpret_cast<const uint32_t*>(dout + base + lane * 2);
-    float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a));
-    float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b));
-    s = x.x * y.x + x.y * y.y;
-    *reinterpret_cast<float2*>(dq_acc + base + lane * 2) = make_float2(0.f, 0.f);
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) Dbuf[(size_t)h * ld + row] = s;
+  for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (ok && sub == 0) Dbuf[(size_t)h * ld + row] = s;
 }
 
 __global__ void convert_dq_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, int64_t begin4,
@@ -737,15 +731,17 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
   if (d != 64 && d != 128) return fail(SKR_E_UNSUPPORTED, "bf16 backward supports d in {64,128}");
   const int rows = row_end - row_begin;
   if (rows > 0) {
-    const int64_t threads = (int64_t)rows * a.hq * 32;
+    const int64_t threads = (int64_t)rows * a.hq * (d / 8);
     const int blocks = (int)((threads + 255) / 256);
     if (d == 128)
       bwd::preprocess_kernel<128><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, (const __nv_bfloat16*)o,
-                                                          (const __nv_bfloat16*)dout, Dbuf, a.ld_lse, dq_acc);
+                                                          (const __nv_bfloat16*)dout, Dbuf, a.ld_lse);
     else
       bwd::preprocess_kernel<64><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, (const __nv_bfloat16*)o,
-                                                         (const __nv_bfloat16*)dout, Dbuf, a.ld_lse, dq_acc);
+                                                         (const __nv_bfloat16*)dout, Dbuf, a.ld_lse);
     if (skr_status e = launch_status("attn bwd preprocess")) return e;
+    if (cudaMemsetAsync(dq_acc + (size_t)row_begin * a.hq * d, 0, (size_t)rows * a.hq * d * 4, st) != cudaSuccess)
+      return fail(SKR_E_CUDA, "attn bwd: dQ accumulator memset");
   }
   if (a.n_tiles > 0) {
     CUtensorMap tq, tk, tv, tdo, tdq;
