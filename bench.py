@@ -64,10 +64,13 @@ def workload(args, world):
     cfg = CONFIGS[name]
     if name == "C2":
         # weak scaling of configs[1]: N x (63 long-tail + one 32K) sequences over the DP x CP grid.
-        # With CP >= 2 the BucketSize is set below the longest sequence (R33) so DACP shards it.
+        # With CP >= 2 the BucketSize is set below the longest sequence (R33) so DACP shards it:
+        # 30720 gives 3 micro-batches per rank with only the 32K sequences sharded at N = 8 and plan
+        # floors 1.006 / 1.070 / 1.088 at N = 2 / 4 / 8 (24576: 4 / 4 / 3 micro-batches, 19 sequences
+        # sharded at N = 8, floors 1.008 / 1.074 / 1.088).
         cp = world // args.dp
         lens = np.concatenate([cfg.lengths(args.seed + r) for r in range(world)])
-        bucket = cfg.bucket if cp == 1 else 24576
+        bucket = cfg.bucket if cp == 1 else 30720
         return name, cfg, np.asarray(lens, np.int64), cfg.shape, cp, bucket
     else:
         lens = cfg.lengths(args.seed)
