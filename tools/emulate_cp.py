@@ -57,6 +57,8 @@ def main():
     ap.add_argument("--schedulers", default="skrull,dacp-only,rr,full-shard")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--weak", type=int, default=0,
+                    help="C2 weak-scaled to N ranks exactly as bench.py --gpus N builds it (N x the batch, C=30720)")
     a = ap.parse_args()
     import torch
     from paper_2505_19609_b200 import skrull as sk
@@ -65,6 +67,12 @@ def main():
     cfg = CONFIGS[a.config]
     lens = cfg.lengths(a.seed)
     N, C, shp = cfg.cp, cfg.bucket, cfg.shape
+    if a.weak:
+        cfg = CONFIGS["C2"]
+        N, shp = a.weak, cfg.shape
+        lens = np.concatenate([cfg.lengths(a.seed + r) for r in range(N)])
+        C = cfg.bucket if N == 1 else 30720
+        a.config = f"C2 weak x{N}"
     shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
     useful = sum(14 * shp.d * shp.hq * int(S) * (int(S) + 1) // 2 for S in lens)
     g = torch.Generator(device="cuda").manual_seed(a.seed)
