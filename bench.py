@@ -241,7 +241,7 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     from paper_2505_19609_b200 import skrull as sk
-    from paper_2505_19609_b200.runtime import RankStep, dp_micro_batches, grid_coords
+    from paper_2505_19609_b200.runtime import BufferPool, RankStep, dp_micro_batches, grid_coords
 
     dp = args.dp
     dp_rank, cp_rank, _ = grid_coords(rank, world, dp)
@@ -268,8 +268,13 @@ def run_ours(args):
     side = torch.cuda.Stream(priority=-1)
     steps = []
     g = torch.Generator(device="cuda")
-    for j, (ml, ma) in enumerate(mbs):
-        rs = RankStep(shape, ml, ma, cp, cp_rank)
+    # the micro-batches run one after another: their working buffers come from one shared pool
+    pool = BufferPool()
+    rsteps = [RankStep(shape, ml, ma, cp, cp_rank, alloc=pool.reserve) for ml, ma in mbs]
+    pool.materialize()
+    for rs in rsteps:
+        rs.rebind(pool.get)
+    for j, rs in enumerate(rsteps):
         if args.exchange == "peer" and comm is not None:
             rs.connect_peer(comm)              # collective inside the CP group
         g.manual_seed(args.seed * 1_000_003 + rank * 1009 + j)
@@ -341,14 +346,17 @@ def run_ours(args):
         h2d = sum(t.numel() * t.element_size() for hs in host for t in hs.values())
         d2h = sum(t.numel() * t.element_size() for o in outs for t in o.values())
         dev_in = [[{k: torch.empty_like(v) for k, v in src.items()} for _, src in steps] for _ in range(2)]
-        stage = [{k: torch.empty_like(o[k], device="cuda") for k in o} for o in outs]
+        # staging for the gradients, double-buffered by step parity (the micro-batches share their
+        # working buffers, so each micro-batch's gradients are staged right after its backward)
+        stage = [[{k: torch.empty_like(o[k], device="cuda") for k in o} for o in outs] for _ in range(2)]
         copy, copy_out = torch.cuda.Stream(), torch.cuda.Stream()   # one per direction (full duplex)
         main = torch.cuda.current_stream()
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]
         ev_used = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_out, ev_out_free = torch.cuda.Event(), torch.cuda.Event()
+        ev_out = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_out_free = [torch.cuda.Event(), torch.cuda.Event()]
         used_rec = [False, False]
-        out_rec = [False]
+        out_rec = [False, False]
 
         def h2d_set(b):
             with torch.cuda.stream(copy):
@@ -366,24 +374,24 @@ def run_ours(args):
                 if k + 1 < n:
                     h2d_set(1 - b)
                 main.wait_event(ev_in[b])
-                for (rs, _), di in zip(steps, dev_in[b]):
+                if out_rec[b]:
+                    main.wait_event(ev_out_free[b])  # the D2H of step k-2 has read this staging set
+                for (rs, _), di, st in zip(steps, dev_in[b], stage[b]):
                     fwd_bwd(rs, di)
-                ev_used[b].record(main)
-                used_rec[b] = True
-                if out_rec[0]:
-                    main.wait_event(ev_out_free)     # the previous D2H has read the staging buffers
-                for (rs, _), st in zip(steps, stage):
                     for kk in st:
                         st[kk].copy_(getattr(rs, kk)[:rs.rows], non_blocking=True)
-                ev_out.record(main)
+                ev_used[b].record(main)
+                used_rec[b] = True
+                ev_out[b].record(main)
                 with torch.cuda.stream(copy_out):
-                    copy_out.wait_event(ev_out)
-                    for st, o in zip(stage, outs):
+                    copy_out.wait_event(ev_out[b])
+                    for st, o in zip(stage[b], outs):
                         for kk in o:
                             o[kk].copy_(st[kk], non_blocking=True)
-                    ev_out_free.record(copy_out)
-                out_rec[0] = True
-            main.wait_event(ev_out_free)
+                    ev_out_free[b].record(copy_out)
+                out_rec[b] = True
+            main.wait_event(ev_out_free[0])
+            main.wait_event(ev_out_free[1])
 
         e2e_run(2)
         torch.cuda.synchronize()

@@ -25,10 +25,46 @@ import torch
 from . import skrull as sk
 
 
+class BufferPool:
+    """Working buffers shared by the micro-batches of one rank, which run one after another (the
+    Eq. 8 sum over micro-batches): every named buffer is ONE flat allocation sized to the
+    largest request, and each RankStep takes views of it. Two phases: RankSteps are built with
+    `reserve` (meta-tensor placeholders), then `materialize()` allocates and `RankStep.rebind(pool.get)`
+    hands out the views. Keeps a rank's memory at one micro-batch's working set (C5 at 256 sequences
+    per GPU needs 57 micro-batches)."""
+
+    def __init__(self, device="cuda"):
+        self.dev, self.need, self.bufs = device, {}, None
+
+    def reserve(self, name, shape, dtype):
+        n = 1
+        for x in shape:
+            n *= int(x)
+        self.need[name] = (max(self.need.get(name, (0, dtype))[0], n), dtype)
+        return torch.empty(shape, dtype=dtype, device="meta")
+
+    def materialize(self):
+        self.bufs = {k: torch.empty(n, dtype=dt, device=self.dev) for k, (n, dt) in self.need.items()}
+
+    def get(self, name, shape, dtype):
+        n = 1
+        for x in shape:
+            n *= int(x)
+        return self.bufs[name][:n].view(*shape)
+
+
+def _alloc_new(device):
+    return lambda name, shape, dtype: torch.empty(*shape, device=device, dtype=dtype)
+
+
 class RankStep:
-    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda"):
+    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda", alloc=None):
+        """alloc(name, shape, dtype) -> tensor: where the working buffers come from (default: fresh
+        allocations; BufferPool.reserve to share them across micro-batches)."""
         self.shape, self.cp, self.rank = shape, cp, rank
         self.dev = device
+        self._alloc = alloc or _alloc_new(device)
+        self._bufspec = []
         hq, hkv, d = shape.hq, shape.hkv, shape.d
         self.dt = torch.bfloat16 if shape.dtype == sk.SKR_BF16 else torch.float32
         pr = sk.skr_pack_rank(mb_lens, assign, cp, rank)
@@ -52,19 +88,34 @@ class RankStep:
             self.chunks = torch.as_tensor(sk.skr_pack_chunks(mb_lens, assign, cp).reshape(-1)).to(device)
         # packed buffers (>= P rows so the all-gather send prefix is always in bounds)
         R = max(self.rows, self.P, 1)
-        e = lambda *s, dt=None: torch.empty(*s, device=device, dtype=dt or self.dt)  # noqa: E731
-        self.q, self.o, self.do, self.dq = (e(R, hq, d) for _ in range(4))
-        self.k, self.v, self.dk, self.dv = (e(R, hkv, d) for _ in range(4))
-        self.lse = torch.empty(hq, R, device=device, dtype=torch.float32)
-        self.ws = torch.empty(sk.skr_attn_bwd_ws_bytes(shape, R) // 4 + 64, device=device, dtype=torch.float32)
+        f32, dt = torch.float32, self.dt
+        for name in ("q", "o", "do", "dq"):
+            self._buf(name, (R, hq, d), dt)
+        for name in ("k", "v", "dk", "dv"):
+            self._buf(name, (R, hkv, d), dt)
+        self._buf("lse", (hq, R), f32)
+        self._buf("ws", (sk.skr_attn_bwd_ws_bytes(shape, R) // 4 + 64,), f32)
         if self.has_dist:
             N, P, nat = cp, self.P, max(self.nat_rows, 1)
-            self.k_gath, self.v_gath = e(N * P, hkv, d), e(N * P, hkv, d)
-            self.k_nat, self.v_nat = e(nat, hkv, d), e(nat, hkv, d)
-            f32 = torch.float32
-            self.dk_nat, self.dv_nat = e(nat, hkv, d, dt=f32), e(nat, hkv, d, dt=f32)
-            self.dk_rm, self.dv_rm = e(N * P, hkv, d, dt=f32), e(N * P, hkv, d, dt=f32)
-            self.dk_red, self.dv_red = e(P, hkv, d, dt=f32), e(P, hkv, d, dt=f32)
+            for name in ("k_gath", "v_gath"):
+                self._buf(name, (N * P, hkv, d), dt)
+            for name in ("k_nat", "v_nat"):
+                self._buf(name, (nat, hkv, d), dt)
+            for name in ("dk_nat", "dv_nat"):
+                self._buf(name, (nat, hkv, d), f32)
+            for name in ("dk_rm", "dv_rm"):
+                self._buf(name, (N * P, hkv, d), f32)
+            for name in ("dk_red", "dv_red"):
+                self._buf(name, (P, hkv, d), f32)
+
+    def _buf(self, name, shape, dtype):
+        self._bufspec.append((name, shape, dtype))
+        setattr(self, name, self._alloc(name, shape, dtype))
+
+    def rebind(self, alloc):
+        """Re-fetch every working buffer from `alloc` (after BufferPool.materialize)."""
+        for name, shape, dtype in self._bufspec:
+            setattr(self, name, alloc(name, shape, dtype))
 
     def launches_per_step(self, exchange="nccl") -> int:
         """Kernels of this library launched by one forward + backward of this micro-batch."""
