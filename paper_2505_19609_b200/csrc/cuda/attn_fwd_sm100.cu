@@ -81,12 +81,17 @@ constexpr int kSoftmax = 256;                // threads per head (two warpgroups
 constexpr int kTmaWarp = 16, kMmaWarp = 17;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
+#ifndef SKR_FWD_BN128
+#define SKR_FWD_BN128 128   // key-tile width of the d = 128 forward (64: separate P columns, see Cfg)
+#endif
+
 template <int D>
 struct Cfg {
+  static constexpr int BN = D == 128 ? SKR_FWD_BN128 : 128;   // keys per K/V tile
   static constexpr int kChunks = D / 64;                 // 64-col SW128 boxes per row
   static constexpr int kQBytes = BM * D * 2;             // one Q tile
   static constexpr int kKVBytes = BN * D * 2;            // one K or V tile
-  static constexpr int kUnits = D == 128 ? 4 : 6;        // K/V ring depth (units of one tile), <= 8
+  static constexpr int kUnits = D == 128 ? (BN == 64 ? 8 : 4) : 6;   // K/V ring depth (tiles), <= 8
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQBytes;
   static constexpr int kOffRed = kOffKV + kUnits * kKVBytes;   // [head][tile parity][half][row] row maxima
@@ -95,10 +100,11 @@ struct Cfg {
   // TMEM columns. P (bf16 pairs) is the A operand of O += P V straight from TMEM (no smem traffic).
   // d = 64 : S_A[0,128) S_B[128,256) O_A[256,320) O_B[320,384) P_A[384,448) P_B[448,512)
   // d = 128: S_A[0,128) S_B[128,256) O_A[256,384) O_B[384,512); P_s aliases the first 64 cols of S_s
-  static constexpr bool kPAlias = D == 128;
-  __device__ static constexpr uint32_t tS(int s) { return s * 128; }
+  // d = 128, BN = 64: S_A[0,64) S_B[64,128) P_A[128,160) P_B[160,192) O_A[256,384) O_B[384,512)
+  static constexpr bool kPAlias = D == 128 && BN == 128;
+  __device__ static constexpr uint32_t tS(int s) { return s * BN; }
   __device__ static constexpr uint32_t tO(int s) { return 256 + s * D; }
-  __device__ static constexpr uint32_t tP(int s) { return kPAlias ? s * 128 : 384 + s * 64; }
+  __device__ static constexpr uint32_t tP(int s) { return kPAlias ? s * 128 : (D == 128 ? 128 + s * 32 : 384 + s * 64); }
 };
 
 struct Bars {  // kUnits <= 8
@@ -114,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
                     const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, int pairs_per_group) {
   using C = Cfg<D>;
+  constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
           }
         }
         l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
-        tmem_st32(tP, pk);
+        tmem_st_half<HN / 2>(tP, pk);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full[s]);
@@ -481,8 +488,10 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   CUtensorMap tq, tk, tv;
   const uint64_t qcols = (uint64_t)a.hq * d, kcols = (uint64_t)a.hkv * d;
   if (!make_tmap_2d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, fwd::BM, 64, true) ||
-      !make_tmap_2d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, fwd::BN, 64, true) ||
-      !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, fwd::BN, 64, true))
+      !make_tmap_2d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols,
+                    d == 128 ? fwd::Cfg<128>::BN : fwd::Cfg<64>::BN, 64, true) ||
+      !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols,
+                    d == 128 ? fwd::Cfg<128>::BN : fwd::Cfg<64>::BN, 64, true))
     return fail(SKR_E_CUDA, "attn fwd: tensor map encode failed");
   const int grp = a.hq / a.hkv;
   const int ppg = (grp + 1) / 2;
