@@ -594,27 +594,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
 #endif
-      // the previous step's reduce must have finished reading the smem tile
-      if (warp == 8 && elect_one()) bulk_wait_read<0>();
-      named_bar_sync(1, 128);
-      pa.mark(1);
       if (D == 128) {
-        // dQ^T: lane = feature t, columns = queries of the step. Element (q, t) of a SW128 box sits at
-        // q * 128 + (((t / 4) ^ (q % 8)) * 16) + (t % 4) * 4: eight per-thread offsets (q % 8) plus
-        // compile-time q * 128 immediates, one STS per element. (Direct red.global from registers
-        // instead of the smem tile + TMA reduce was measured 1.5x slower for the whole kernel.)
-        uint32_t off[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m)
-          off[m] = sDQ + (t / 32) * kBoxBytes + ((((t % 32) >> 2) ^ m) << 4) + (t & 3) * 4;
+        // dQ^T: lane = feature t, columns = queries of the step. Staged as two 16 KB halves (queries
+        // [0,32) and [32,64)), each four SW128 boxes [32 q][32 f], double-buffered so the stores of
+        // one half overlap the TMA reduce of the other (and of the previous step): the dQ
+        // warpgroup's store -> reduce -> tile-free chain was the d = 128 critical path
+        // (profiles/r01_experiments.md). Element (q, t) of a box sits at q * 128 + (((t / 4) ^
+        // (q % 8)) * 16) + (t % 4) * 4: eight per-thread offsets (q % 8) plus q * 128 immediates.
         uint32_t r[BQ / 32][32];
 #pragma unroll
         for (int c = 0; c < BQ; c += 32) tmem_ld32(tmem + lane_base + C::tDQ + c, r[c / 32]);
         tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bars->dq_empty);              // the step's dQ^T is in registers
+        pa.mark(1);
+        constexpr int kHalfBytes = 32 * D * 4, kHBox = 32 * 128;
 #pragma unroll
-        for (int q = 0; q < BQ; ++q)
-          st_shared_f32(off[q % 8] + q * 128, __uint_as_float(r[q / 32][q % 32]) * a.scale);
+        for (int hh = 0; hh < BQ / 32; ++hh) {
+          // the reduce that last read this half (two bulk groups ago) must be done
+          if (warp == 8 && elect_one()) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+          const uint32_t hb = sDQ + hh * kHalfBytes + (t / 32) * kHBox + (t & 3) * 4;
+          uint32_t off[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) off[m] = hb + ((((t % 32) >> 2) ^ m) << 4);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) st_shared_f32(off[q % 8] + q * 128, __uint_as_float(r[hh][q]) * a.scale);
+          fence_async_smem();
+          named_bar_sync(1, 128);
+          if (warp == 8) {
+            if (elect_one()) {
+              if (q0 + 32 * hh < q_len) {            // rows past the segment would only add zeros
+#pragma unroll
+                for (int b = 0; b < D / 32; ++b)
+                  tma_reduce_add_2d(&tm_dq, smem + C::kOffDQ + hh * kHalfBytes + b * kHBox, h * D + b * 32,
+                                    cu0 + q0 + 32 * hh);
+              }
+              bulk_commit();                           // one group per half, empty or not
+            }
+            __syncwarp();
+          }
+        }
+        pa.mark(2);
       } else {
+        // the previous step's reduce must have finished reading the smem tile
+        if (warp == 8 && elect_one()) bulk_wait_read<0>();
+        named_bar_sync(1, 128);
+        pa.mark(1);
         // dQ: lane = query row t, columns = features
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
@@ -627,21 +653,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                          __uint_as_float(r[i + 1]) * a.scale, __uint_as_float(r[i + 2]) * a.scale,
                          __uint_as_float(r[i + 3]) * a.scale);
         }
-      }
-      tc_fence_before();
-      mbar_arrive(&bars->dq_empty);                // TMEM dQ columns may be overwritten
-      pa.mark(2);
-      if (t == 0) trace(21);
-      fence_async_smem();
-      named_bar_sync(1, 128);
-      if (warp == 8) {
-        if (elect_one()) {
+        tc_fence_before();
+        mbar_arrive(&bars->dq_empty);                // TMEM dQ columns may be overwritten
+        pa.mark(2);
+        if (t == 0) trace(21);
+        fence_async_smem();
+        named_bar_sync(1, 128);
+        if (warp == 8) {
+          if (elect_one()) {
 #pragma unroll
-          for (int b = 0; b < kBoxes; ++b)
-            tma_reduce_add_2d(&tm_dq, smem + C::kOffDQ + b * kBoxBytes, h * D + b * 32, cu0 + q0);
-          bulk_commit();
+            for (int b = 0; b < kBoxes; ++b)
+              tma_reduce_add_2d(&tm_dq, smem + C::kOffDQ + b * kBoxBytes, h * D + b * 32, cu0 + q0);
+            bulk_commit();
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       pa.mark(3);
     }
@@ -751,7 +777,8 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
         !make_tmap_2d(&tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_q_rows, qcols, qcols, bq, 64, true) ||
         !make_tmap_2d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true) ||
         !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, bwd::BN, 64, true) ||
-        !make_tmap_2d(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n_q_rows, qcols, qcols, bq, 32, true))
+        !make_tmap_2d(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n_q_rows, qcols, qcols,
+                      d == 128 ? 32 : bq, 32, true))   // d = 128 reduces in 32-query halves
       return fail(SKR_E_CUDA, "attn bwd: tensor map encode failed");
     dim3 grid(a.hkv, a.n_tiles);
     // share of exponentials on the FMA pipe; SKR_BWD_POLY (0-3) overrides for sweeps
