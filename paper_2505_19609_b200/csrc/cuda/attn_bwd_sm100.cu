@@ -87,16 +87,26 @@ struct Cfg {
   //  d = 128: S^T[0,64) dP^T[64,128) dQ^T[128,192) P^T[192,224) dS^T[224,256) dV[256,384) dK[384,512)
   //  d =  64: S^T[0,128) dP^T[128,256) dQ[256,320) dV[320,384) dK[384,448) P^T[448,512);
   //           dS^T aliases dP^T: warpgroup w packs its 64 columns into [128+64w, 160+64w)
+  //  d = 128 with kKT: K^T (bf16 pairs, lanes = features) is the TMEM A operand of dQ^T = K^T dS^T
+  //           at [192,256), P^T / dS^T alias the warpgroup's own S^T / dP^T columns:
+  //           S^T[0,64) (P^T at 32w) dP^T[64,128) (dS^T at 64+32w) dQ^T[128,192) K^T[192,256) dV dK
   static constexpr bool kDSAlias = D == 64;
+#ifndef SKR_BWD_KT
+#define SKR_BWD_KT 0   // measured slower (profiles/r01_experiments.md); kept as an option
+#endif
+  static constexpr bool kKT = D == 128 && SKR_BWD_KT;
   static constexpr int tS = 0;
   static constexpr int tDP = BQ;
   static constexpr int tDQ = 2 * BQ;
   static constexpr int tDV = D == 128 ? 256 : 320;
   static constexpr int tDK = 384;
   static constexpr int tPT = D == 128 ? 192 : 448;
+  static constexpr int tKT = 192;
   // packed column of query pair-column q/2 for P^T / dS^T, per warpgroup half
-  __device__ static constexpr int tDS(int w) { return kDSAlias ? 128 + 64 * w : 224 + (H / 2) * w; }
-  __device__ static constexpr int tPTw(int w) { return tPT + (H / 2) * w; }
+  __device__ static constexpr int tDS(int w) {
+    return kDSAlias ? 128 + 64 * w : (kKT ? BQ + H * w : 224 + (H / 2) * w);
+  }
+  __device__ static constexpr int tPTw(int w) { return kKT ? H * w : tPT + (H / 2) * w; }
 };
 
 struct Bars {
@@ -105,6 +115,7 @@ struct Bars {
   uint64_t s_full, dp_full, p_full, ds_full, dv_done, dsq_done, dq_full, dq_empty;
   uint64_t s_free, dp_free;
   uint64_t mma_done;   // single phase: every MMA of the CTA has completed (dK / dV epilogue)
+  uint64_t kt_full;    // kKT: K^T written to TMEM by the dQ warpgroup (128 arrivals)
   uint32_t tmem_base;
 };
 
@@ -158,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->s_free, kComputeThreads);
     mbar_init(&bars->dp_free, kComputeThreads);
     mbar_init(&bars->mma_done, 1);
+    mbar_init(&bars->kt_full, 128);
     fence_mbar_init();
   }
   trace_init();
@@ -296,11 +308,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_f16_ts(tmem + tcol, tmem + a_col, b_desc + ((uint32_t)(k * 2048) >> 4), id_kv, acc || k > 0);
       }
     };
+    const uint32_t id_dq_ts = idesc_bf16_f32(D, BQ, 0, 1);   // kKT: A = K^T from TMEM, B = dS^T (MN-major)
     auto issue_dq = [&]() {
 #pragma unroll
       for (int k = 0; k < BN / 16; ++k) {
         const uint32_t o = (uint32_t)(k * 2048) >> 4;
-        if (D == 128)
+        if (C::kKT)
+          umma_f16_ts(tmem + C::tDQ, tmem + C::tKT + k * 8, dDS0 + o, id_dq_ts, k > 0);
+        else if (D == 128)
           umma_f16(tmem + C::tDQ, dKmn + o, dDS0 + o, id_dq, k > 0);
         else
           umma_f16(tmem + C::tDQ, dDSmn + o, dK0 + o, id_dq, k > 0);
@@ -320,10 +335,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&bars->s_full);
       issue_t(dV, dDO, C::tDP, 1);
       umma_commit(&bars->dp_full);
-      // S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T has its
-      // own columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it follows
-      // dK(n) in the in-order tensor pipe.
-      for (int n = 0; n < n_steps; ++n) {
+      // kKT (d = 128): P^T / dS^T alias S^T / dP^T, so S(n+1) follows dV(n) and dP(n+1) follows dK(n)
+      // in the in-order tensor pipe (p_full / ds_full also mean the compute warpgroups read S / dP).
+      // Otherwise S(n+1) is issued as soon as the compute warpgroups have read S(n) out of TMEM (P^T
+      // has its own columns); dP(n+1) likewise for d = 128, while for d = 64 (dS^T aliases dP^T) it
+      // follows dK(n).
+      for (int n = 0; C::kKT && n < n_steps; ++n) {
+        const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
+        const bool more = n + 1 < n_steps;
+        pa.mark(6);
+        mbar_wait_sleep(&bars->p_full, n & 1);
+        pa.mark(2);
+        tc_fence_after();
+        issue_kv(false, dDOmn + st * qstage, C::tDV, n > 0);
+        umma_commit(&bars->dv_done);
+        if (more) {
+          pa.mark(6);
+          mbar_wait_sleep(&bars->qdo_full[st1], ((n + 1) / C::kStages) & 1);
+          pa.mark(1);
+          tc_fence_after();
+          issue_t(dK, dQ + st1 * qstage, C::tS, 2 * st1);
+          umma_commit(&bars->s_full);
+        }
+        pa.mark(6);
+        mbar_wait_sleep(&bars->ds_full, n & 1);
+        pa.mark(4);
+        tc_fence_after();
+        issue_kv(true, dQmn + st * qstage, C::tDK, n > 0);
+        if (more) {
+          issue_t(dV, dDO + st1 * qstage, C::tDP, 2 * st1 + 1);
+          umma_commit(&bars->dp_full);
+        }
+        pa.mark(6);
+        if (n == 0) mbar_wait_sleep(&bars->kt_full, 0);
+        mbar_wait_sleep(&bars->dq_empty, (n & 1) ^ 1);
+        pa.mark(5);
+        tc_fence_after();
+        issue_dq();
+        umma_commit(&bars->dq_full);
+        umma_commit(&bars->dsq_done);
+        umma_commit(&bars->qdo_empty[st]);
+      }
+      for (int n = 0; !C::kKT && n < n_steps; ++n) {
         const int st = n % C::kStages, st1 = (n + 1) % C::kStages;
         const bool more = n + 1 < n_steps;
         pa.mark(6);
@@ -565,6 +618,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sDQ = smem_u32(smem + C::kOffDQ);
     constexpr int kBoxes = D / 32;                 // 32-column fp32 boxes
     constexpr int kBoxBytes = BQ * 128;
+    if (C::kKT) {
+      // K^T into TMEM (lane = feature t, packed key pairs): the A operand of every dQ^T MMA
+      mbar_wait(&bars->kv_full, 0);
+      const uint32_t kb = smem_u32(smem + C::kOffK) + (t / 64) * (BN * 128);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = 2 * (32 * c + i);
+          const uint32_t lo = ld_shared_u16(kb + sw128_off(key, t % 64));
+          const uint32_t hi = ld_shared_u16(kb + sw128_off(key + 1, t % 64));
+          pk[i] = lo | (hi << 16);
+        }
+        tmem_st32(tmem + lane_base + C::tKT + 32 * c, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bars->kt_full);
+    }
     StepIter it(qt_first, qt_last);
     PhaseAcct pa;   // 0 wait dQ, 1 wait smem tile free, 2 TMEM -> smem, 3 issue reduce
     pa.start();
