@@ -481,11 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           e0 = fmul2(make_float2(p[i], p[i + 1]), sl2_2);
           e1 = fmul2(make_float2(p[i + 2], p[i + 3]), sl2_2);
         } else {
-#ifdef SKR_EXP_NO_LDS   // timing experiment only (wrong results): LSE / D loads removed
-          const float4 l4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
-#else
           const float4 l4 = ld_shared_f4(a_lse + i * 4);     // -lse2 is folded: p * sl2 - lse2
-#endif
           e0 = ffma2(make_float2(p[i], p[i + 1]), sl2_2, make_float2(-l4.x, -l4.y));
           e1 = ffma2(make_float2(p[i + 2], p[i + 3]), sl2_2, make_float2(-l4.z, -l4.w));
         }
@@ -541,11 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               float2 t0 = make_float2(__uint_as_float(r[b][i]), __uint_as_float(r[b][i + 1]));
               float2 t1 = make_float2(__uint_as_float(r[b][i + 2]), __uint_as_float(r[b][i + 3]));
               if (!C::kInit) {   // kInit: the accumulator already holds dP - D
-#ifdef SKR_EXP_NO_LDS
-                const float4 d4 = make_float4(sl2, sl2 * 0.5f, sl2 * 0.25f, sl2 * 2.f);
-#else
                 const float4 d4 = ld_shared_f4(a_dd + (c + i) * 4);
-#endif
                 t0 = fadd2(t0, make_float2(-d4.x, -d4.y));
                 t1 = fadd2(t1, make_float2(-d4.z, -d4.w));
               }
@@ -647,26 +639,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       pa.mark(0);
       if (t == 0) trace(20);
       tc_fence_after();
-#if defined(SKR_EXP_NO_DQ) || defined(SKR_EXP_DQ_RED)   // timing experiments
-      if (D == 128) {
-        uint32_t r[BQ / 32][32];
-#pragma unroll
-        for (int c = 0; c < BQ; c += 32) tmem_ld32(tmem + lane_base + C::tDQ + c, r[c / 32]);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&bars->dq_empty);
-#ifdef SKR_EXP_DQ_RED
-        const int nv = min(BQ, q_len - q0);
-        float* base = dq_acc + ((size_t)(cu0 + q0) * a.hq + h) * D + t;
-#pragma unroll
-        for (int q = 0; q < BQ; ++q)
-          if (q < nv) red_add_f32(base + (size_t)q * a.hq * D, __uint_as_float(r[q / 32][q % 32]) * a.scale);
-#else
-        if (__uint_as_float(r[0][0]) == 1234.5f) dq_acc[t] = 0.f;
-#endif
-        continue;
-      }
-#endif
       if (D == 128) {
         // dQ^T: lane = feature t, columns = queries of the step. Staged as two 16 KB halves (queries
         // [0,32) and [32,64)), each four SW128 boxes [32 q][32 f], double-buffered so the stores of

@@ -91,7 +91,10 @@ struct Cfg {
   static constexpr int kChunks = D / 64;                 // 64-col SW128 boxes per row
   static constexpr int kQBytes = BM * D * 2;             // one Q tile
   static constexpr int kKVBytes = BN * D * 2;            // one K or V tile
-  static constexpr int kUnits = D == 128 ? (BN == 64 ? 8 : 4) : 6;   // K/V ring depth (tiles), <= 8
+#ifndef SKR_FWD_UNITS64
+#define SKR_FWD_UNITS64 6
+#endif
+  static constexpr int kUnits = D == 128 ? (BN == 64 ? 8 : 4) : SKR_FWD_UNITS64;   // K/V ring depth (tiles), <= 8
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQBytes;
   static constexpr int kOffRed = kOffKV + kUnits * kKVBytes;   // [head][tile parity][half][row] row maxima
