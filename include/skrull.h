@@ -239,6 +239,48 @@ skr_status skr_comm_reduce_scatter_f32(skr_comm* c, const float* send, float* re
                                        void* stream);
 skr_status skr_comm_all_reduce_f32(skr_comm* c, float* buf, size_t count, void* stream);
 
+/* ------------------------------------------------------------------ a5-a9 as one call per direction
+ * The CP-rank step of one micro-batch (Eq. 2, mirrored for the
+ * backward, reading R24), sequenced on a main and a side stream:
+ *  fwd: main packs Q/K/V; side all-gathers the K/V distributed prefix (NCCL, CP group) and reorders
+ *       it to natural order; main runs the LOCAL tiles meanwhile, then waits and runs the DISTRIBUTED
+ *       chunks.
+ *  bwd: main packs dO, zeroes the fp32 partials and runs the DISTRIBUTED chunks; side permutes,
+ *       reduce-scatters (sum) and casts into the packed dK/dV prefix while main runs the LOCAL tiles;
+ *       main then waits for the side stream (the call returns with all work ordered on `main`).
+ * With natural_rows == 0 no collective is issued and `comm` may be null. All buffers are caller-owned
+ * device memory laid out as DESIGN.md §2 describes; the tables come from skr_pack_rank /
+ * skr_pack_chunks / skr_tiles_*. */
+typedef struct skr_attn_plan skr_attn_plan;   /* opaque: shape + packed-buffer row capacity */
+skr_status skr_attn_plan_create(const skr_attn_shape* s, int32_t max_rows, skr_attn_plan** out);
+void skr_attn_plan_destroy(skr_attn_plan* p);
+typedef struct {
+  skr_segs local_fwd, local_bwd, dist_fwd, dist_bwd; /* segment classes with their work lists */
+  const int32_t* chunk_table;   /* [n_chunks * 6] (skr_pack_chunks), device */
+  int32_t n_chunks;
+  int32_t cp;                   /* CP group size N */
+  int32_t rows;                 /* packed rows of this rank */
+  int32_t dist_rows;            /* rows of the distributed prefix (all-gather send rows) */
+  int32_t pad_rows_P;           /* P = max over ranks of dist_rows (R22) */
+  int32_t natural_rows;         /* rows of the natural distributed-K/V buffer */
+  int32_t buf_rows;             /* rows allocated in q/k/v/o/dout/dq/dk/dv/lse (>= max(rows, P)) */
+  const int32_t* src_row;       /* [rows] packed row -> rank-natural input row (skr_pack_rank) */
+  const void *q_src, *k_src, *v_src, *do_src;     /* rank-natural inputs */
+  void *q, *k, *v, *o, *dout, *dq, *dk, *dv;      /* packed, [buf_rows][h][d] */
+  float* lse;                                     /* [hq][buf_rows] */
+  void *k_gathered, *v_gathered;                  /* [cp*P][hkv][d] */
+  void *k_natural, *v_natural;                    /* [natural_rows][hkv][d], kept from fwd to bwd */
+  float *dk_partial, *dv_partial;                 /* [natural_rows][hkv][d] fp32 */
+  float *dk_rankmajor, *dv_rankmajor;             /* [cp*P][hkv][d] fp32 (reduce-scatter input) */
+  float *dk_reduced, *dv_reduced;                 /* [P][hkv][d] fp32 (reduce-scatter output) */
+  void* ws;                                       /* skr_attn_bwd workspace for buf_rows */
+  size_t ws_bytes;
+} skr_cp_step;
+skr_status skr_cp_attn_fwd(skr_comm* comm, const skr_attn_plan* plan, const skr_cp_step* step, void* main_stream,
+                           void* side_stream);
+skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan, const skr_cp_step* step, void* main_stream,
+                           void* side_stream);
+
 /* ------------------------------------------------------------------ diagnostics */
 /* UMMA/TMA/TMEM building-block self-test: C[128][n] fp32 from bf16 A/B with operand layout
  * `variant` (0: A K-major, B K-major; 1: B MN-major; 2: A and B MN-major; 3: A written by threads

@@ -108,6 +108,23 @@ class RankStep:
             for name in ("dk_red", "dv_red"):
                 self._buf(name, (P, hkv, d), f32)
 
+    def cp_step(self, q_src, k_src, v_src, do_src):
+        """The skr_cp_step of this micro-batch (row a5-a9 composite C-ABI call) for these inputs."""
+        if getattr(self, "_plan", None) is None:
+            self._plan = sk.AttnPlan(self.shape, self.q.shape[0])
+        p = lambda t: t.data_ptr() if t is not None else 0  # noqa: E731
+        d = self.has_dist
+        return sk.skr_cp_step(
+            self.loc_f.struct(), self.loc_b.struct(), self.dist_f.struct(), self.dist_b.struct(),
+            p(self.chunks) if d else 0, self.n_chunks if d else 0, self.cp, self.rows, self.dist_rows, self.P,
+            self.nat_rows, self.q.shape[0], p(self.src_row),
+            p(q_src), p(k_src), p(v_src), p(do_src),
+            p(self.q), p(self.k), p(self.v), p(self.o), p(self.do), p(self.dq), p(self.dk), p(self.dv), p(self.lse),
+            p(self.k_gath) if d else 0, p(self.v_gath) if d else 0, p(self.k_nat) if d else 0,
+            p(self.v_nat) if d else 0, p(self.dk_nat) if d else 0, p(self.dv_nat) if d else 0,
+            p(self.dk_rm) if d else 0, p(self.dv_rm) if d else 0, p(self.dk_red) if d else 0,
+            p(self.dv_red) if d else 0, p(self.ws), self.ws.numel() * 4)
+
     def _buf(self, name, shape, dtype):
         self._bufspec.append((name, shape, dtype))
         setattr(self, name, self._alloc(name, shape, dtype))
@@ -195,7 +212,31 @@ class RankStep:
                                                    self.lse, self.dq, self.dk, self.dv, 0, self.ws, stream), stream)
 
     # ------------------------------------------------------------------ production composition
+    # One C-ABI call per direction (skr_cp_attn_fwd / _bwd, csrc/cuda/cp_step.cu). The per-phase
+    # composition below runs the same kernels call by call; it is used when the attention calls are
+    # timed individually (self.events) and by the one-GPU loopback tests.
     def forward(self, q_src, k_src, v_src, comm=None, side=None):
+        if self.events is None:
+            self._fwd_inputs = (q_src, k_src, v_src)
+            sk.skr_cp_attn_fwd(comm, self._plan_or_new(), self.cp_step(q_src, k_src, v_src, None),
+                               torch.cuda.current_stream(), side or torch.cuda.current_stream())
+            return
+        self.forward_phases(q_src, k_src, v_src, comm, side)
+
+    def backward(self, do_src, comm=None, side=None):
+        if self.events is None:
+            q_src, k_src, v_src = getattr(self, "_fwd_inputs", (None, None, None))
+            sk.skr_cp_attn_bwd(comm, self._plan_or_new(), self.cp_step(q_src, k_src, v_src, do_src),
+                               torch.cuda.current_stream(), side or torch.cuda.current_stream())
+            return
+        self.backward_phases(do_src, comm, side)
+
+    def _plan_or_new(self):
+        if getattr(self, "_plan", None) is None:
+            self._plan = sk.AttnPlan(self.shape, self.q.shape[0])
+        return self._plan
+
+    def forward_phases(self, q_src, k_src, v_src, comm=None, side=None):
         main = torch.cuda.current_stream()
         self.pack_qkv(q_src, k_src, v_src)
         if self.has_dist:
@@ -214,7 +255,7 @@ class RankStep:
             main.wait_event(ev_kv)
             self.fwd_dist()
 
-    def backward(self, do_src, comm=None, side=None):
+    def backward_phases(self, do_src, comm=None, side=None):
         main = torch.cuda.current_stream()
         self.pack_do(do_src)
         if self.has_dist:

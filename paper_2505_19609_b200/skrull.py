@@ -423,6 +423,42 @@ def skr_cast_f32_bf16(src, dst, stream=None):
     _check(fn(_tptr(src), _tptr(dst), src.numel(), _stream(stream)))
 
 
+# ---------------------------------------------------------------------------- a5-a9 composite step
+class skr_cp_step(C.Structure):
+    _fields_ = [("local_fwd", skr_segs), ("local_bwd", skr_segs), ("dist_fwd", skr_segs), ("dist_bwd", skr_segs),
+                ("chunk_table", vp), ("n_chunks", i32), ("cp", i32), ("rows", i32), ("dist_rows", i32),
+                ("pad_rows_P", i32), ("natural_rows", i32), ("buf_rows", i32), ("src_row", vp),
+                ("q_src", vp), ("k_src", vp), ("v_src", vp), ("do_src", vp),
+                ("q", vp), ("k", vp), ("v", vp), ("o", vp), ("dout", vp), ("dq", vp), ("dk", vp), ("dv", vp),
+                ("lse", vp), ("k_gathered", vp), ("v_gathered", vp), ("k_natural", vp), ("v_natural", vp),
+                ("dk_partial", vp), ("dv_partial", vp), ("dk_rankmajor", vp), ("dv_rankmajor", vp),
+                ("dk_reduced", vp), ("dv_reduced", vp), ("ws", vp), ("ws_bytes", C.c_size_t)]
+
+
+class AttnPlan:
+    """skr_attn_plan wrapper (opaque: shape + packed-buffer row capacity)."""
+
+    def __init__(self, shape, max_rows):
+        self.h = vp()
+        _check(_sig("skr_attn_plan_create", i32, P(skr_attn_shape), i32, P(vp))(C.byref(shape), int(max_rows),
+                                                                               C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            _sig("skr_attn_plan_destroy", None, vp)(self.h)
+            self.h = vp()
+
+
+def skr_cp_attn_fwd(comm, plan, step, main=None, side=None):
+    _check(_sig("skr_cp_attn_fwd", i32, vp, vp, P(skr_cp_step), vp, vp)(
+        comm.h if comm is not None else None, plan.h, C.byref(step), _stream(main), _stream(side)))
+
+
+def skr_cp_attn_bwd(comm, plan, step, main=None, side=None):
+    _check(_sig("skr_cp_attn_bwd", i32, vp, vp, P(skr_cp_step), vp, vp)(
+        comm.h if comm is not None else None, plan.h, C.byref(step), _stream(main), _stream(side)))
+
+
 # ---------------------------------------------------------------------------- f3: peer-memory exchange
 def skr_ipc_blob_bytes() -> int:
     return _sig("skr_ipc_blob_bytes", i32)()
