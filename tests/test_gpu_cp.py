@@ -116,3 +116,44 @@ def test_peer_exchange_loopback(case):
     else:
         n_dist, _ = _run([3, 5, 2, 700, 800, 1, 7], 14, 2, 64, 4, 400, True, 3, exchange="peer")
     assert n_dist >= 1
+
+
+def test_buffer_pool_micro_batches_share_buffers():
+    # GDS splits this batch into several micro-batches; their RankSteps take views of ONE BufferPool
+    # (bench.py's memory layout) and run one after another through the composite C-ABI step
+    # (skr_cp_attn_fwd / _bwd, N = 1); each micro-batch is read back right after its backward.
+    from paper_2505_19609_b200 import skrull as sk
+    from paper_2505_19609_b200.runtime import BufferPool, RankStep, gather_rank_natural
+    lens = [900, 37, 700, 129, 1, 600, 64, 1000, 250, 333]
+    hq, hkv, d = 8, 2, 64
+    shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16)
+    p = sk.skr_plan(lens, 1200, 1, 1, hq * d, hkv * d)
+    n_mb = int(p["n_mb_per_dp"][0])
+    assert n_mb >= 3
+    inputs = make_inputs(lens, hq, hkv, d, seed=9, bf16=True)
+    pool = BufferPool()
+    mbs = []
+    for j in range(n_mb):
+        idx = np.nonzero(p["mb_of_seq"] == j)[0]
+        ml, ma = np.asarray(lens)[idx], p["assign"][idx]
+        mbs.append((idx, ml, ma, RankStep(shape, ml, ma, 1, 0, alloc=pool.reserve)))
+    pool.materialize()
+    for *_, rs in mbs:
+        rs.rebind(pool.get)
+    assert len({rs.q.data_ptr() for *_, rs in mbs}) == 1          # one shared working set
+    for idx, ml, ma, rs in mbs:
+        mb_inputs = [inputs[i] for i in idx]
+        src = {k: torch.from_numpy(gather_rank_natural(mb_inputs, ml, ma, 1, 0, k)).to("cuda", torch.bfloat16)
+               for k in ("q", "k", "v", "do")}
+        rs.forward(src["q"], src["k"], src["v"])
+        rs.backward(src["do"])
+        torch.cuda.synchronize()
+        pr = rs.pr
+        for i in range(pr["n_seg"]):
+            a, b = pr["cu_seqlens_q"][i], pr["cu_seqlens_q"][i + 1]
+            x = inputs[idx[pr["seg_seq"][i]]]
+            O, _ = attn_fwd(x["q"], x["k"], x["v"])
+            dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
+            for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
+                ok, err, bound = tol_ok(getattr(rs, key)[a:b].float().cpu().numpy(), ref, False)
+                assert ok, f"{key} seq {idx[pr['seg_seq'][i]]}: err {err} > {bound}"
