@@ -166,6 +166,30 @@ def ncu_traffic(workload, world, kind):
         return None
 
 
+def eval_prediction(sk, all_mbs, cp, bucket, shp):
+    """Row f2: the paper's evaluator (Eq. 8 = max over DP ranks of the sum over micro-batches of
+    Eq. 1's TDACP, skr_eval_tdacp) with the B200 T_comp fit of profiles/r01_calibration.json (against
+    Eq. 12's FLOPs, as the paper fits it) and Table 5's all-gather fit for T_comm (no
+    NVLink sweep yet), in ms -- printed next to the measured step. None without a calibration."""
+    names = {(14, 2, 64): "qwen05", (28, 4, 128): "qwen7", (32, 8, 128): "llama8"}
+    path = os.path.join(ROOT, "profiles", "r01_calibration.json")
+    name = names.get((shp.hq, shp.hkv, shp.d))
+    if not name or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        fit = json.load(f)["t_comp"][name]["fit_eq12"]
+    comp = (fit["slope_s_per_flop"], fit["intercept_s"])
+    comm = (6.256e-6 / (1 << 20), 116.5e-6)          # Table 5 all_gather, per byte (R25: 2 B/elem)
+    worst = 0.0
+    for d_mbs in all_mbs:
+        t = 0.0
+        for ml, ma in d_mbs:
+            r = sk.skr_eval_tdacp(ml, ma, bucket, cp, shp.hidden, shp.kv_hidden, comp, comm, bytes_per_elem=2.0)
+            t += r["tdacp"]
+        worst = max(worst, t)
+    return worst * 1e3
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 def cpu_oracle_sample(lens, shape: Shape, seconds: float, seed: int = 0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: sequences taken
@@ -444,6 +468,7 @@ def run_ours(args):
             t_dp.append(sum(max(p) for p in pp))
             tot += sum(sum(p) for p in pp)
         floor = max(t_dp) / max(1e-9, tot / world)
+        predicted = eval_prediction(sk, all_mbs, cp, bucket, shp)
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -470,6 +495,7 @@ def run_ours(args):
             "clocks": clocks,
             "max_mean_rank_time": step_ms / mean_rank,
             "plan_floor": floor,
+            "eval_predicted_ms": predicted,
             "plan_us": plan_us,
             "fwd_ms": float(allv[:, 1].max()), "bwd_ms": float(allv[:, 2].max()),
         }
