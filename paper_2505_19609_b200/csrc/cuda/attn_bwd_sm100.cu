@@ -415,6 +415,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace(4);
         tc_fence_after();
         issue_kv(true, dQmn + st * qstage, C::tDK, n > 0);
+        // d = 64 (dS^T aliases dP^T): dP(n+1) may follow dK(n), the last reader of dS^T(n) in TMEM
+        // (dQ(n) reads dS from smem), so it goes into the pipe before dQ(n) and its dq_empty wait
+        if (C::kDSAlias && more) {
+          issue_t(dV, dDO + st1 * qstage, C::tDP, 2 * st1 + 1);
+          umma_commit(&bars->dp_full);
+        }
         pa.mark(6);
         mbar_wait_sleep(&bars->dq_empty, (n & 1) ^ 1);
         pa.mark(5);
@@ -424,10 +430,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bars->dq_full);
         umma_commit(&bars->dsq_done);
         umma_commit(&bars->qdo_empty[st]);
-        if (C::kDSAlias && more) {
-          issue_t(dV, dDO + st1 * qstage, C::tDP, 2 * st1 + 1);
-          umma_commit(&bars->dp_full);
-        }
       }
       umma_commit(&bars->mma_done);
       pa.mark(6);
