@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qp_base = q_pos + it.qt * BQ + col0;        // position of this warpgroup's first query
       const bool diag = kv0 + BN - 1 > qp_base;             // warp-uniform: causal mask needed
       mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1);
+      if (threadIdx.x == 0) trace(14);
       const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (C::kStages * BQ + st * BQ + col0) * 4;
       mbar_wait(&bars->s_full, n & 1);
       pa.mark(0);

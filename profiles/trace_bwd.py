@@ -31,7 +31,7 @@ ev = np.array([(x >> 48, x & ((1 << 48) - 1)) for x in buf[:n] if x])
 ev = ev[np.argsort(ev[:, 1], kind="stable")]
 t0 = ev[0, 1]
 names = {1: "M s_free", 2: "M qdo", 3: "M p_full", 4: "M ds_full", 5: "M dq_empty", 10: "C s_full", 11: "C p_arrive",
-         12: "C dp_full", 13: "C ds_arrive", 20: "Q dq_full", 21: "Q dq_empty_arr"}
+         12: "C dp_full", 13: "C ds_arrive", 14: "C qdo_full", 20: "Q dq_full", 21: "Q dq_empty_arr"}
 lo = int(sys.argv[2]) if len(sys.argv) > 2 else 0          # optional window start (cycles after t0)
 sel = [(e, t) for e, t in ev if t - t0 >= lo][:200]
 for e, t in sel:
