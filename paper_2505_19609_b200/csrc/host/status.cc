@@ -38,4 +38,4 @@ SKR_EXPORT const char* skr_status_string(skr_status s) {
 
 SKR_EXPORT const char* skr_last_error(void) { return skr::g_err; }
 
-SKR_EXPORT int32_t skr_abi_version(void) { return 1; }
+SKR_EXPORT int32_t skr_abi_version(void) { return 2; }   // 2: cp_step, attn_plan, peer exchange
