@@ -458,6 +458,253 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------------------------
+// d = 128, one q-head per CTA ("1h"): TMEM S0 [0,128) S1 [128,256) P [256,320) O [384,512). With
+// one head the S accumulator can be DOUBLE-buffered and P gets its own columns, so S(j+1) is
+// computed while the softmax works on S(j) and PV(j) overlaps the exponentials of j+1 -- the
+// two-head kernel's per-head chain S(j) -> softmax -> PV(j) -> S(j+1) (P aliasing S) is gone.
+// Four softmax warpgroups split the 128 key columns (32 each) and combine row maxima through smem.
+// The cost: K/V tiles are loaded and read per head (no GQA sharing inside the CTA).
+struct Cfg1h {
+  static constexpr int D = 128, kChunks = 2;
+  static constexpr int kQBytes = BM * D * 2, kKVBytes = 128 * D * 2;
+  static constexpr int kUnits = 5;
+  static constexpr int kOffQ = 0, kOffKV = kQBytes;
+  static constexpr int kOffRed = kOffKV + kUnits * kKVBytes;        // [parity][4][BM] maxima, then [4][BM] sums
+  static constexpr int kOffBar = kOffRed + (2 * 4 + 4) * BM * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static constexpr uint32_t tS(int b) { return b * 128; }
+  static constexpr uint32_t tP = 256, tO = 384;
+};
+
+struct Bars1h {
+  uint64_t q_full;
+  uint64_t kv_full[8], kv_empty[8];
+  uint64_t s_full[2], s_free[2], p_full, pv_done;
+  uint32_t tmem_base;
+};
+
+template <int kPolyPer8>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd1h_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
+                      float* __restrict__ lse) {
+  using C = Cfg1h;
+  constexpr int D = 128, BN = 128, HN = 32;            // key columns per softmax warpgroup
+  constexpr int kSm = 4 * 128;                         // softmax threads of the head
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars1h* bars = reinterpret_cast<Bars1h*>(smem + C::kOffBar);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  const int h = blockIdx.x, g = h / (a.hq / a.hkv);
+  const int seg = a.tiles[2 * blockIdx.y], tile = a.tiles[2 * blockIdx.y + 1];
+  const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
+  const int r0 = cu0 + tile * BM;
+  const int n_valid = min(BM, cu1 - r0);
+  const int qp0 = a.q_pos[seg] + tile * BM;
+  const int n_kv = (qp0 + n_valid + BN - 1) / BN;
+  const int kst = a.k_start[seg];
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
+    for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&bars->s_full[b], 1), mbar_init(&bars->s_free[b], kSm);
+    mbar_init(&bars->p_full, kSm);
+    mbar_init(&bars->pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == kTmaWarp) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_expect_tx(&bars->q_full, C::kQBytes);
+      for (int c = 0; c < C::kChunks; ++c)
+        tma_load_2d(smem + C::kOffQ + c * (BM * 128), &tm_q, &bars->q_full, h * D + c * 64, r0);
+    }
+    __syncwarp();
+    int it = 0;
+    for (int j = 0; j < n_kv; ++j) {
+      for (int kv = 0; kv < 2; ++kv, ++it) {
+        const int u = it % C::kUnits;
+        mbar_wait_sleep(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(&bars->kv_full[u], C::kKVBytes);
+          uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_2d(dst + c * (BN * 128), kv == 0 ? &tm_k : &tm_v, &bars->kv_full[u], g * D + c * 64,
+                        kst + j * BN);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (elect_one()) {
+      const uint32_t id_s = idesc_bf16_f32(BM, BN, 0, 0), id_o = idesc_bf16_f32(BM, D, 0, 1);
+      const uint64_t dq0 = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
+      const uint64_t dkv0 = sdesc_sw128(smem_u32(smem + C::kOffKV), 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(smem_u32(smem + C::kOffKV), BN * 128, 1024);
+      auto kunit = [&](int j) { return (2 * j) % C::kUnits; };
+      auto vunit = [&](int j) { return (2 * j + 1) % C::kUnits; };
+      mbar_wait_sleep(&bars->q_full, 0);
+      tc_fence_after();
+      // S(j) into buffer j & 1 as soon as K(j) is in and the softmax has read S(j-2); then PV(j-1)
+      // once P(j-1) is stored: S(j) overlaps softmax(j-1), PV(j-1) overlaps the exps of j
+      for (int j = 0; j <= n_kv; ++j) {
+        if (j < n_kv) {
+          mbar_wait_sleep(&bars->kv_full[kunit(j)], ((2 * j) / C::kUnits) & 1);
+          if (j >= 2) mbar_wait_sleep(&bars->s_free[j & 1], ((j - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint64_t dk = dkv0 + ((uint32_t)(kunit(j) * C::kKVBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = ((k / 4) * (BM * 128) + (k % 4) * 32) >> 4;
+            const uint32_t koff = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
+            umma_f16(tmem + C::tS(j & 1), dq0 + off, dk + koff, id_s, k > 0);
+          }
+          umma_commit(&bars->s_full[j & 1]);
+          umma_commit(&bars->kv_empty[kunit(j)]);
+        }
+        if (j > 0) {
+          const int jv = j - 1;
+          mbar_wait_sleep(&bars->kv_full[vunit(jv)], ((2 * jv + 1) / C::kUnits) & 1);
+          mbar_wait_sleep(&bars->p_full, jv & 1);
+          tc_fence_after();
+          const uint64_t dv = dv0 + ((uint32_t)(vunit(jv) * C::kKVBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < BN / 16; ++k)
+            umma_f16_ts(tmem + C::tO, tmem + C::tP + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, jv > 0 || k > 0);
+          umma_commit(&bars->pv_done);
+          umma_commit(&bars->kv_empty[vunit(jv)]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int w = warp / 4;                  // key-column quarter [32w, 32w + 32)
+    const int row = (warp % 4) * 32 + lane;
+    const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
+    const uint32_t tO = tmem + lane_base + C::tO + w * (D / 4);
+    const uint32_t tP = tmem + lane_base + C::tP + w * (HN / 2);
+    float* red = reinterpret_cast<float*>(smem + C::kOffRed);           // [parity][4][BM]
+    float* lsum = red + 2 * 4 * BM;                                     // [4][BM]
+    const int qp = qp0 + row;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait(&bars->s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      float x[HN];
+      {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + C::tS(b) + w * HN, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->s_free[b]);          // S buffer b may take S(j + 2)
+      const int kv0 = j * BN + w * HN;
+      if (kv0 + HN - 1 > qp0) {
+#pragma unroll
+        for (int i = 0; i < HN; ++i)
+          if (kv0 + i > qp) x[i] = -INFINITY;
+      }
+      float mxs[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mxs[i] = fmax3(x[i], x[i + 8], x[i + 16]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mxs[i] = fmaxf(mxs[i], x[i + 24]);
+      float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                       fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+      float* rj = red + b * (4 * BM);
+      rj[w * BM + row] = mx;
+      named_bar_sync(1, kSm);
+      mx = fmaxf(fmaxf(rj[row], rj[BM + row]), fmaxf(rj[2 * BM + row], rj[3 * BM + row]));
+      const float m_new = fmaxf(m_ref, mx * sl2);
+      const bool rescale = __any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0;
+      const float alpha = (rescale && j > 0) ? ex2(m_ref - m_new) : 1.f;
+      if (rescale) m_ref = m_new;
+      const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+      uint32_t pk[HN / 2];
+#pragma unroll
+      for (int c = 0; c < HN; c += 8) {
+        float pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const float2 xx = ffma2(make_float2(x[c + i], x[c + i + 1]), sl2_2, nm2);
+          pv[i] = i < kPolyPer8 ? ex2_poly(xx.x) : ex2(xx.x);
+          pv[i + 1] = i + 1 < kPolyPer8 ? ex2_poly(xx.y) : ex2(xx.y);
+          ls2[(i / 2) % 2] = fadd2(ls2[(i / 2) % 2], make_float2(pv[i], pv[i + 1]));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
+      }
+      // PV(j-1) must have consumed P and finished accumulating O before P / O are touched
+      if (j > 0) {
+        mbar_wait(&bars->pv_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (rescale && j > 0) {
+#pragma unroll
+        for (int c = 0; c < D / 4; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(tO + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float2 v = fmul2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                   make_float2(alpha, alpha));
+            r[i] = __float_as_uint(v.x), r[i + 1] = __float_as_uint(v.y);
+          }
+          tmem_st16(tO + c, r);
+        }
+      }
+      l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y));
+      tmem_st16(tP, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+    }
+    // epilogue: combine the quarters' row sums, O / l -> bf16 (this quarter's 32 d columns), LSE
+    lsum[w * BM + row] = l;
+    named_bar_sync(1, kSm);
+    l = (lsum[row] + lsum[BM + row]) + (lsum[2 * BM + row] + lsum[3 * BM + row]);
+    mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    uint32_t r[32];
+    tmem_ld32(tO, r);
+    tmem_wait_ld();
+    if (row < n_valid) {
+      __nv_bfloat16* orow = out + ((size_t)(r0 + row) * a.hq + h) * D + w * (D / 4);
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 v;
+        v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+        v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+        v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+        v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+        *reinterpret_cast<uint4*>(orow + i) = v;
+      }
+      if (w == 0) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace fwd
 
 static unsigned long long* fwd_trace_buffer() {
@@ -512,6 +759,24 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
   };
+  // d = 128, one head per CTA (double-buffered S, separate P): opt-in, SKR_FWD_1H=1 (measured slower:
+  // without the GQA head pair each K/V tile is loaded and read per head, profiles/r01_experiments.md)
+  static int one_head = [] {
+    const char* e = getenv("SKR_FWD_1H");
+    return e ? atoi(e) : 0;
+  }();
+  if (d == 128 && one_head) {
+    constexpr int smem = fwd::Cfg1h::kSmem;
+    dim3 g1(a.hq, a.n_tiles);
+    auto launch1 = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kern<<<g1, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse);
+    };
+    if (pp == 0) launch1(fwd::attn_fwd1h_kernel<0>);
+    else if (pp == 1) launch1(fwd::attn_fwd1h_kernel<1>);
+    else launch1(fwd::attn_fwd1h_kernel<2>);
+    return launch_status("attn_fwd1h_kernel");
+  }
   if (d == 128) {
     constexpr int smem = fwd::Cfg<128>::kSmem;
     switch (pp) {
