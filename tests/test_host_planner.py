@@ -216,3 +216,28 @@ def test_baselines_bit_exact_fuzz():
     with pytest.raises(skrull.SkrullError):
         skrull.skr_round_robin([50, 60, 90], 100, 2, rollback=False)
     assert list(skrull.skr_round_robin([50, 60, 90], 100, 2)[0]).count(-1) >= 1
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    # the boundary is a C ABI: include/skrull.h compiles as strict C99 and a plain C program links
+    # against libskrull.so and calls through it (host planner entry points need no GPU)
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    from paper_2505_19609_b200 import skrull
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "abi.c"
+    src.write_text('#include "skrull.h"\n#include <stdio.h>\n'
+                   'int main(void) {\n'
+                   '  skr_model m = {64, 16, 1}; int64_t f = 0;\n'
+                   '  if (skr_flops(128, &m, &f) != SKR_OK) return 1;\n'
+                   '  printf("%d %lld\\n", (int)skr_abi_version(), (long long)f);\n'
+                   '  return 0;\n}\n')
+    lib_dir = os.path.dirname(skrull.LIB_PATH)
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(root, "include"),
+                    str(src), "-L", lib_dir, "-l:" + os.path.basename(skrull.LIB_PATH), "-Wl,-rpath," + lib_dir,
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert int(out[0]) == skrull.skr_abi_version() and int(out[1]) == 15204352
