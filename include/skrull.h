@@ -160,7 +160,10 @@ typedef struct {                /* one segment class (locals, or distributed chu
   int32_t row_begin, row_end;   /* host ints: the class's packed query rows are [row_begin, row_end) */
 } skr_segs;
 
-/* Forward (row a7; Eq. 2-4): per segment and q-head h (kv head h*hkv/hq),
+/* Input contract of the attention calls: every row of q / k / v (and dout) inside
+ * [0, n_q_rows) / [0, n_kv_rows) must be finite, also rows no segment owns -- a 128-row tile reads
+ * past a segment's end and the tensor cores multiply those rows by exact zeros (0 x NaN = NaN).
+ * Forward (row a7; Eq. 2-4): per segment and q-head h (kv head h*hkv/hq),
  * O = softmax(scale QK^T + bottom-right causal mask) V, LSE = natural-log row logsumexp.
  * q, o: [n_q_rows][hq][d]; k, v: [n_kv_rows][hkv][d]; lse: fp32 [hq][n_q_rows].
  * bf16 in/out with fp32 accumulation (SKR_BF16) or fp32 throughout (SKR_FP32).
@@ -266,7 +269,9 @@ typedef struct {
   int32_t buf_rows;             /* rows allocated in q/k/v/o/dout/dq/dk/dv/lse (>= max(rows, P)) */
   const int32_t* src_row;       /* [rows] packed row -> rank-natural input row (skr_pack_rank) */
   const void *q_src, *k_src, *v_src, *do_src;     /* rank-natural inputs */
-  void *q, *k, *v, *o, *dout, *dq, *dk, *dv;      /* packed, [buf_rows][h][d] */
+  void *q, *k, *v, *o, *dout, *dq, *dk, *dv;      /* packed, [buf_rows][h][d]; rows [rows, buf_rows)
+                                                     must hold FINITE values (e.g. zeros): attention
+                                                     tiles read them and multiply them by exact zeros */
   float* lse;                                     /* [hq][buf_rows] */
   void *k_gathered, *v_gathered;                  /* [cp*P][hkv][d] */
   void *k_natural, *v_natural;                    /* [natural_rows][hkv][d], kept from fwd to bwd */

@@ -44,7 +44,10 @@ class BufferPool:
         return torch.empty(shape, dtype=dtype, device="meta")
 
     def materialize(self):
-        self.bufs = {k: torch.empty(n, dtype=dt, device=self.dev) for k, (n, dt) in self.need.items()}
+        # zero-filled: rows past a micro-batch's own rows are read by attention tiles (and multiplied
+        # by exact zeros), so they must hold finite values -- zeros here, finite data of a larger
+        # micro-batch later
+        self.bufs = {k: torch.zeros(n, dtype=dt, device=self.dev) for k, (n, dt) in self.need.items()}
 
     def get(self, name, shape, dtype):
         n = 1
@@ -54,7 +57,9 @@ class BufferPool:
 
 
 def _alloc_new(device):
-    return lambda name, shape, dtype: torch.empty(*shape, device=device, dtype=dtype)
+    # zero-filled for the same reason as BufferPool.materialize: padding rows [rows, max(rows, P))
+    # enter the attention tiles and must be finite (0 x NaN would poison dK / dQ / O)
+    return lambda name, shape, dtype: torch.zeros(*shape, device=device, dtype=dtype)
 
 
 class RankStep:
