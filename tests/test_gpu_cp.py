@@ -175,4 +175,5 @@ def test_random_plans_fuzz(case):
     lens = [int(min(3000, max(1, rng.lognormvariate(5.0, 1.4)))) for _ in range(K)]
     lo = max(max(lens) // N + 1, 64)
     C = rng.randint(lo, max(lo, sum(lens) // N + 256))
-    _run(lens, hq, hkv, d, N, C, case % 6 != 5, 50 + case)   # every 6th case in fp32 test mode
+    # every 6th case in fp32 test mode; every 3rd through the row-f3 peer-memory exchange
+    _run(lens, hq, hkv, d, N, C, case % 6 != 5, 50 + case, exchange="peer" if case % 3 == 1 else "nccl")
