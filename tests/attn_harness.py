@@ -96,3 +96,28 @@ def local_pack(inputs, torch_dtype):
         base[s] = r
         r += S
     return Packed(inputs, segs, base, list(range(len(inputs))), torch_dtype)
+
+
+def bf16_model_bwd(x, scale=None):
+    """Test-side model of the kernels' documented precision (R31), NOT the oracle: the plain
+    backward with P and dS rounded to bf16 where they enter the tensor-core GEMMs, D computed
+    from the bf16-stored O, and dQ / dK / dV rounded to the bf16 they are stored in. Used to bound the error of stress inputs (peaky logits), whose gradient
+    error is dominated by exactly these roundings. fp64 torch on CPU; returns dQ, dK, dV."""
+    import torch
+    q, k, v, do = (torch.tensor(np.asarray(x[n]), dtype=torch.float64) for n in ("q", "k", "v", "do"))
+    S, hq, d = q.shape
+    hkv = k.shape[1]
+    sc = 1.0 / np.sqrt(d) if scale is None else scale
+    rb = lambda t: t.to(torch.bfloat16).to(torch.float64)  # noqa: E731
+    mask = torch.tril(torch.ones(S, S, dtype=torch.bool))
+    dQ, dK, dV = torch.zeros_like(q), torch.zeros_like(k), torch.zeros_like(v)
+    for h in range(hq):
+        g = (h * hkv) // hq
+        A = (sc * q[:, h] @ k[:, g].T).masked_fill(~mask, float("-inf"))
+        P = torch.softmax(A, dim=1)
+        D = (do[:, h] * rb(P @ v[:, g])).sum(1, keepdim=True)
+        dS = P * (do[:, h] @ v[:, g].T - D)
+        dV[:, g] += rb(P).T @ do[:, h]
+        dQ[:, h] = sc * rb(dS) @ k[:, g]
+        dK[:, g] += sc * rb(dS).T @ q[:, h]
+    return rb(dQ).numpy(), rb(dK).numpy(), rb(dV).numpy()

@@ -147,6 +147,36 @@ def test_bwd_bf16_local_ragged(hq, hkv, d):
     _check_bwd_local(pk, dQ, dK, dV, fp32=False)
 
 
+@pytest.mark.parametrize("hq,hkv,d", SHAPES[:2])
+def test_bwd_bf16_peaky_softmax(hq, hkv, d):
+    # sigma 3 Q/K: large logits and LSE magnitudes through the backward -- for d = 64 the -LSE/scale
+    # and -D values enter the accumulators as 3-term bf16 splits (one K = 16 MMA each), which must
+    # keep full fp32 precision at these magnitudes. With logits of std ~9 the gradients reach ~20
+    # and their error is dominated by the bf16 rounding of P and dS where they enter the GEMMs
+    # (R31): the bound is the error of that rounding model (tests/attn_harness.bf16_model_bwd)
+    # against the exact oracle, x1.25, + 2e-2 -- a kernel bug (a wrong split, a dropped term) would
+    # exceed it by orders of magnitude.
+    from tests.attn_harness import bf16_model_bwd
+    sk = _sk()
+    lens = [700, 1500, 129]
+    inputs = make_inputs(lens, hq, hkv, d, seed=7, sigma_qk=3.0)
+    pk = local_pack(inputs, torch.bfloat16)
+    shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16)
+    O, L, dQ, dK, dV = _run_bwd(sk, shape, pk)
+    _check_fwd(pk, O, L, fp32=False)
+    r = 0
+    for s_, lo, hi in pk.segs:
+        _, _, rq, rk, rv = oracle_seq(pk.inputs[s_])
+        mq, mk, mv = bf16_model_bwd(pk.inputs[s_])
+        n = hi - lo
+        for name, got, ref, model in (("dQ", dQ[r:r + n], rq, mq), ("dK", dK[r:r + n], rk, mk),
+                                      ("dV", dV[r:r + n], rv, mv)):
+            env = np.abs(model - ref).max()
+            err = np.abs(got - ref).max()
+            assert err <= 1.25 * env + 2e-2, f"{name} seq {s_}: err {err} > 1.25 x model {env} + 2e-2"
+        r += n
+
+
 def test_bwd_fp32_local():
     sk = _sk()
     lens = [1, 33, 64, 90, 200, 300]
