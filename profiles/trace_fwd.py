@@ -30,6 +30,7 @@ names = {1: "M S_A done", 2: "M S_B done", 3: "M PV_A done", 4: "M PV_B done", 5
          13: "A p_arrive", 40: "T K issue", 41: "T V issue", 9: "M K ready, S busy", 60: "M PVA wait V", 61: "M PVB wait V", 62: "M PVA wait P", 63: "M PVB wait P", 64: "M S_A wait K", 65: "M S_B wait K", 66: "M S_A wait free", 67: "M S_B wait free", 30: "A w0 s_free", 31: "A w1 s_free", 32: "A w2 s_free", 33: "A w3 s_free", 34: "A w0 p_full", 35: "A w1 p_full", 36: "A w2 p_full", 37: "A w3 p_full", 50: "B w0 s_free", 51: "B w1 s_free", 52: "B w2 s_free", 53: "B w3 s_free", 54: "B w0 p_full", 55: "B w1 p_full", 56: "B w2 p_full", 57: "B w3 p_full", 20: "B s_full", 21: "B exps_done", 22: "B pv_done", 23: "B p_arrive"}
 kinds = ["s_full", "s_free", "exps", "pv_done", "p_full"]
 lo = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+print(f"{len(ev)} events")
 for e, t, j in ev[lo:lo + 600]:
     e = int(e)
     if 30 <= e < 35 or 50 <= e < 55:   # per-warp softmax events: j | warp << 6
