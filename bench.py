@@ -307,12 +307,17 @@ def run_ours(args):
                for k, hh in (("q", shp.hq), ("k", shp.hkv), ("v", shp.hkv), ("do", shp.hq))}
         steps.append((rs, src))
 
-    def fwd_bwd(rs, src):
+    def fwd_bwd(rs, src, ev_do=None):
+        # ev_do (e2e only): the backward waits for this micro-batch's dO copy, the forward does not
         if args.exchange == "peer" and comm is not None:
             rs.forward_peer(src["q"], src["k"], src["v"], side)
+            if ev_do is not None:
+                torch.cuda.current_stream().wait_event(ev_do)
             rs.backward_peer(src["do"], side)
         else:
             rs.forward(src["q"], src["k"], src["v"], comm, side)
+            if ev_do is not None:
+                torch.cuda.current_stream().wait_event(ev_do)
             rs.backward(src["do"], comm, side)
 
     def one_step():
@@ -375,7 +380,11 @@ def run_ours(args):
         stage = [[{k: torch.empty_like(o[k], device="cuda") for k in o} for o in outs] for _ in range(2)]
         copy, copy_out = torch.cuda.Stream(), torch.cuda.Stream()   # one per direction (full duplex)
         main = torch.cuda.current_stream()
-        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        # per input set and micro-batch: one event once its Q, K, V are in (the forward may start),
+        # one once its dO is in (the backward may start)
+        n_mb = len(steps)
+        ev_qkv = [[torch.cuda.Event() for _ in range(n_mb)] for _ in range(2)]
+        ev_do = [[torch.cuda.Event() for _ in range(n_mb)] for _ in range(2)]
         ev_used = [torch.cuda.Event(), torch.cuda.Event()]
         ev_out = [torch.cuda.Event(), torch.cuda.Event()]
         ev_out_free = [torch.cuda.Event(), torch.cuda.Event()]
@@ -386,10 +395,12 @@ def run_ours(args):
             with torch.cuda.stream(copy):
                 if used_rec[b]:
                     copy.wait_event(ev_used[b])      # the step that last read this set is done
-                for hs, di in zip(host, dev_in[b]):
-                    for k in hs:
+                for m, (hs, di) in enumerate(zip(host, dev_in[b])):
+                    for k in ("q", "k", "v"):
                         di[k].copy_(hs[k], non_blocking=True)
-                ev_in[b].record(copy)
+                    ev_qkv[b][m].record(copy)
+                    di["do"].copy_(hs["do"], non_blocking=True)
+                    ev_do[b][m].record(copy)
 
         def e2e_run(n):
             h2d_set(0)
@@ -397,11 +408,11 @@ def run_ours(args):
                 b = k % 2
                 if k + 1 < n:
                     h2d_set(1 - b)
-                main.wait_event(ev_in[b])
                 if out_rec[b]:
                     main.wait_event(ev_out_free[b])  # the D2H of step k-2 has read this staging set
-                for (rs, _), di, st in zip(steps, dev_in[b], stage[b]):
-                    fwd_bwd(rs, di)
+                for m, ((rs, _), di, st) in enumerate(zip(steps, dev_in[b], stage[b])):
+                    main.wait_event(ev_qkv[b][m])
+                    fwd_bwd(rs, di, ev_do[b][m])
                     for kk in st:
                         st[kk].copy_(getattr(rs, kk)[:rs.rows], non_blocking=True)
                 ev_used[b].record(main)
