@@ -3,6 +3,7 @@
 #include "device.cuh"
 
 namespace skr {
+bool fwd_two_sm();   // attn_fwd_sm100.cu: d = 128 forward on CTA pairs (SKR_FWD_2SM=1)
 skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k, const void* v, void* o, float* lse,
                           int n_q_rows, int n_kv_rows, cudaStream_t st);
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
@@ -43,7 +44,10 @@ static AttnArgs make_args(const skr_attn_shape* s, const skr_segs* g, int ld_lse
 
 using namespace skr;
 
-SKR_EXPORT int32_t skr_attn_block_m(const skr_attn_shape* s) { return (s && s->dtype == SKR_FP32) ? 32 : 128; }
+SKR_EXPORT int32_t skr_attn_block_m(const skr_attn_shape* s) {
+  if (s && s->dtype == SKR_FP32) return 32;
+  return (s && s->d == 128 && fwd_two_sm()) ? 256 : 128;   // a CTA pair takes 256 query rows
+}
 SKR_EXPORT int32_t skr_attn_block_n(const skr_attn_shape* s) { return (s && s->dtype == SKR_FP32) ? 32 : 128; }
 
 SKR_EXPORT size_t skr_attn_bwd_ws_bytes(const skr_attn_shape* s, int32_t n_q_rows) {

@@ -705,6 +705,272 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// d = 128, one q-head per CTA PAIR ("2sm", cta_group::2, opt-in SKR_FWD_2SM=1): the cluster's two
+// CTAs take query tiles 2t and 2t + 1 of one segment (a 256-row super tile of the work list) and
+// run one M = 256 MMA stream issued by the leader.
+// Each CTA holds its 128 Q rows, HALF of every K tile (64 keys: S's B operand is split by N) and
+// HALF of every V tile (64 of the d columns: PV's B operand), so per CTA the shared-memory operand
+// and TMA bytes per KV tile are 96 KB instead of the 1h kernel's 160 KB, with the 1h kernel's
+// double-buffered S and separate P (TMEM S0 [0,128) S1 [128,256) P [256,320) O [384,512) in BOTH
+// CTAs). Hand-overs: TMA completions and the softmax's s_free / p_full arrivals of both CTAs land
+// on the leader's barriers (shared::cluster addresses); the leader's commits multicast to both.
+struct Cfg2sm {
+  static constexpr int D = 128;
+  static constexpr int kQBytes = BM * D * 2;                 // this CTA's 128 query rows
+  static constexpr int kKVBytes = 16384;                     // K: 64 keys x 128 d; V: 128 keys x 64 d
+  static constexpr int kUnits = 8;
+  static constexpr int kOffQ = 0, kOffKV = kQBytes;
+  static constexpr int kOffRed = kOffKV + kUnits * kKVBytes;
+  static constexpr int kOffBar = kOffRed + (2 * 4 + 4) * BM * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static constexpr uint32_t tS(int b) { return b * 128; }
+  static constexpr uint32_t tP = 256, tO = 384;
+};
+
+template <int kPolyPer8>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    attn_fwd2sm_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
+                       float* __restrict__ lse) {
+  using C = Cfg2sm;
+  constexpr int D = 128, BN = 128, HN = 64;            // key columns per softmax warpgroup (two halves)
+  constexpr int kSm = 2 * 128;
+  constexpr int kTma = 8, kMma = 9;
+  constexpr int kArrivals = 2 * 8;                     // s_free / p_full: one per softmax warp of both CTAs
+  // work list entries are 256-row super tiles (skr_attn_block_m = 256 in this mode): CTA r of the
+  // pair takes the super tile's 128-row tile 2t + r
+  const int seg = a.tiles[2 * blockIdx.y], tile0 = 2 * a.tiles[2 * blockIdx.y + 1];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars1h* bars = reinterpret_cast<Bars1h*>(smem + C::kOffBar);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+
+  const int h = blockIdx.x >> 1, g = h / (a.hq / a.hkv);
+  const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
+  const int rs0 = cu0 + tile0 * BM;                     // first row of the super tile
+  const int n_valid_pair = min(2 * BM, cu1 - rs0);
+  const int n_kv = (a.q_pos[seg] + tile0 * BM + n_valid_pair + BN - 1) / BN;   // same in both CTAs
+  const int r0 = rs0 + (int)rank * BM;                  // this CTA's rows
+  const int n_valid = min(BM, cu1 - r0);               // may be <= 0 for rank 1
+  const int qp0 = a.q_pos[seg] + (tile0 + (int)rank) * BM;
+  const int kst = a.k_start[seg];
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
+    for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&bars->s_full[b], 1), mbar_init(&bars->s_free[b], kArrivals);
+    mbar_init(&bars->p_full, kArrivals);
+    mbar_init(&bars->pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == kMma) tmem_alloc_pair<512>(&bars->tmem_base);
+  tc_fence_before();
+  cluster_sync_all();                                   // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == kTma) {
+    const uint32_t q_full_l = mapa_shared(&bars->q_full, 0);
+    if (elect_one()) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      if (leader) mbar_expect_tx(&bars->q_full, 2 * C::kQBytes);
+      for (int c = 0; c < 2; ++c)
+        tma_load_2d_pair(smem + C::kOffQ + c * (BM * 128), &tm_q, q_full_l, h * D + c * 64, r0);
+    }
+    __syncwarp();
+    int it = 0;
+    for (int j = 0; j < n_kv; ++j) {
+      for (int kv = 0; kv < 2; ++kv, ++it) {
+        const int u = it % C::kUnits;
+        mbar_wait_sleep(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(&bars->kv_full[u], 2 * C::kKVBytes);
+          const uint32_t full_l = mapa_shared(&bars->kv_full[u], 0);
+          uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
+          if (kv == 0) {   // K rows [64 rank, 64 rank + 64) of the tile, both 64-column chunks of d
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_pair(dst + c * (64 * 128), &tm_k, full_l, g * D + c * 64, kst + j * BN + 64 * (int)rank);
+          } else {         // V: all 128 keys, d columns [64 rank, 64 rank + 64)
+            tma_load_2d_pair(dst, &tm_v, full_l, g * D + 64 * (int)rank, kst + j * BN);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == kMma) {
+    if (leader && elect_one()) {
+      const uint32_t id_s = idesc_bf16_f32(2 * BM, BN, 0, 0), id_o = idesc_bf16_f32(2 * BM, D, 0, 1);
+      const uint64_t dq0 = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
+      const uint64_t dkv0 = sdesc_sw128(smem_u32(smem + C::kOffKV), 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(smem_u32(smem + C::kOffKV), 128 * 128, 1024);
+      auto kunit = [&](int j) { return (2 * j) % C::kUnits; };
+      auto vunit = [&](int j) { return (2 * j + 1) % C::kUnits; };
+      mbar_wait_sleep(&bars->q_full, 0);
+      tc_fence_after();
+      for (int j = 0; j <= n_kv; ++j) {
+        if (j < n_kv) {
+          mbar_wait_sleep(&bars->kv_full[kunit(j)], ((2 * j) / C::kUnits) & 1);
+          if (j >= 2) mbar_wait_sleep(&bars->s_free[j & 1], ((j - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint64_t dk = dkv0 + ((uint32_t)(kunit(j) * C::kKVBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = ((k / 4) * (BM * 128) + (k % 4) * 32) >> 4;
+            const uint32_t koff = ((k / 4) * (64 * 128) + (k % 4) * 32) >> 4;
+            umma2_f16(tmem + C::tS(j & 1), dq0 + off, dk + koff, id_s, k > 0);
+          }
+          umma2_commit_both(&bars->s_full[j & 1]);
+          umma2_commit_both(&bars->kv_empty[kunit(j)]);
+        }
+        if (j > 0) {
+          const int jv = j - 1;
+          mbar_wait_sleep(&bars->kv_full[vunit(jv)], ((2 * jv + 1) / C::kUnits) & 1);
+          mbar_wait_sleep(&bars->p_full, jv & 1);
+          tc_fence_after();
+          const uint64_t dv = dv0 + ((uint32_t)(vunit(jv) * C::kKVBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < BN / 16; ++k)
+            umma2_f16_ts(tmem + C::tO, tmem + C::tP + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, jv > 0 || k > 0);
+          umma2_commit_both(&bars->pv_done);
+          umma2_commit_both(&bars->kv_empty[vunit(jv)]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int w = warp / 4;                  // key-column half [64w, 64w + 64)
+    const int row = (warp % 4) * 32 + lane;
+    const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
+    const uint32_t tO = tmem + lane_base + C::tO + w * (D / 2);
+    const uint32_t tP = tmem + lane_base + C::tP + w * (HN / 2);
+    const uint32_t s_free_l[2] = {mapa_shared(&bars->s_free[0], 0), mapa_shared(&bars->s_free[1], 0)};
+    const uint32_t p_full_l = mapa_shared(&bars->p_full, 0);
+    const uint32_t red = smem_u32(smem + C::kOffRed);                 // [parity][2][BM] maxima, [2][BM] sums
+    const int qp = qp0 + row;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait(&bars->s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      float x[HN];
+      {
+        uint32_t r[2][32];
+        tmem_ld32(tmem + lane_base + C::tS(b) + w * HN, r[0]);
+        tmem_ld32(tmem + lane_base + C::tS(b) + w * HN + 32, r[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[32 * c + i] = __uint_as_float(r[c][i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(s_free_l[b]);   // S buffer b may take S(j + 2)
+      const int kv0 = j * BN + w * HN;
+      if (kv0 + HN - 1 > qp0) {
+#pragma unroll
+        for (int i = 0; i < HN; ++i)
+          if (kv0 + i > qp) x[i] = -INFINITY;
+      }
+      float mxs[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mxs[i] = x[i];
+#pragma unroll
+      for (int i = 8; i < HN; i += 16)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mxs[t] = fmax3(mxs[t], x[i + t], i + 8 + t < HN ? x[i + 8 + t] : x[i + t]);
+      float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                       fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+      const uint32_t rj = red + 4 * (b * 2 * BM);
+      st_shared_f32(rj + 4 * (w * BM + row), mx);
+      named_bar_sync(1, kSm);
+      mx = fmaxf(mx, ld_shared_f32(rj + 4 * ((1 - w) * BM + row)));
+      const float m_new = fmaxf(m_ref, mx * sl2);
+      const bool rescale = __any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0;
+      const float alpha = (rescale && j > 0 && m_ref != -INFINITY) ? ex2(m_ref - m_new) : 1.f;
+      if (rescale) m_ref = m_new;
+      const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+      uint32_t pk[HN / 2];
+#pragma unroll
+      for (int c = 0; c < HN; c += 8) {
+        float pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const float2 xx = ffma2(make_float2(x[c + i], x[c + i + 1]), sl2_2, nm2);
+          pv[i] = i < kPolyPer8 ? ex2_poly(xx.x) : ex2(xx.x);
+          pv[i + 1] = i + 1 < kPolyPer8 ? ex2_poly(xx.y) : ex2(xx.y);
+          ls2[(i / 2) % 2] = fadd2(ls2[(i / 2) % 2], make_float2(pv[i], pv[i + 1]));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
+      }
+      if (j > 0) {
+        mbar_wait(&bars->pv_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (rescale && j > 0) {
+#pragma unroll
+        for (int c = 0; c < D / 2; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(tO + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float2 v = fmul2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                   make_float2(alpha, alpha));
+            r[i] = __float_as_uint(v.x), r[i + 1] = __float_as_uint(v.y);
+          }
+          tmem_st16(tO + c, r);
+        }
+      }
+      l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y));
+      tmem_st32(tP, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(p_full_l);
+    }
+    const uint32_t lsum = red + 4 * (2 * 2 * BM);
+    st_shared_f32(lsum + 4 * (w * BM + row), l);
+    named_bar_sync(1, kSm);
+    l += ld_shared_f32(lsum + 4 * ((1 - w) * BM + row));
+    mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+#pragma unroll
+    for (int c = 0; c < D / 2; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tO + c, r);
+      tmem_wait_ld();
+      if (row < n_valid) {
+        __nv_bfloat16* orow = out + ((size_t)(r0 + row) * a.hq + h) * D + w * (D / 2) + c;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+          v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+          v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+          v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+          *reinterpret_cast<uint4*>(orow + i) = v;
+        }
+      }
+    }
+    if (row < n_valid && w == 0) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  cluster_sync_all();                                   // no arrival or MMA still targets either CTA
+  if (warp == kMma) tmem_dealloc_pair<512>(tmem);
+}
+
 }  // namespace fwd
 
 static unsigned long long* fwd_trace_buffer() {
@@ -729,6 +995,14 @@ extern "C" __attribute__((visibility("default"))) int skr_debug_fwd_trace(unsign
   cudaMemcpy(out, buf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   cudaMemset(buf, 0, 8192 * sizeof(unsigned long long));
   return n;
+}
+
+bool fwd_two_sm() {
+  static const bool on = [] {
+    const char* e = getenv("SKR_FWD_2SM");
+    return e && atoi(e) != 0;
+  }();
+  return on;
 }
 
 skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k, const void* v, void* o, float* lse,
@@ -765,6 +1039,22 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
     const char* e = getenv("SKR_FWD_1H");
     return e ? atoi(e) : 0;
   }();
+  // d = 128, one head per CTA PAIR (cta_group::2): opt-in, SKR_FWD_2SM=1
+  if (d == 128 && fwd_two_sm()) {
+    CUtensorMap tk2;   // K tiles are loaded in halves of 64 keys (one per CTA of the pair)
+    if (!make_tmap_2d(&tk2, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols, 64, 64, true))
+      return fail(SKR_E_CUDA, "attn fwd 2sm: tensor map encode failed");
+    constexpr int smem = fwd::Cfg2sm::kSmem;
+    dim3 g2(2 * a.hq, a.n_tiles);
+    auto launch2 = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kern<<<g2, 320, smem, st>>>(tq, tk2, tv, a, (__nv_bfloat16*)o, lse);
+    };
+    if (pp == 0) launch2(fwd::attn_fwd2sm_kernel<0>);
+    else if (pp == 1) launch2(fwd::attn_fwd2sm_kernel<1>);
+    else launch2(fwd::attn_fwd2sm_kernel<2>);
+    return launch_status("attn_fwd2sm_kernel");
+  }
   if (d == 128 && one_head) {
     constexpr int smem = fwd::Cfg1h::kSmem;
     dim3 g1(a.hq, a.n_tiles);
