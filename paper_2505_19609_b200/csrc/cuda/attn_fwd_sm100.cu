@@ -726,7 +726,15 @@ struct Cfg2sm {
   static constexpr int kOffBar = kOffRed + (2 * 4 + 4) * BM * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr uint32_t tS(int b) { return b * 128; }
-  static constexpr uint32_t tP = 256, tO = 384;
+  static constexpr uint32_t tP(int b) { return 256 + b * 64; }   // P double-buffered: P(j) may be
+  static constexpr uint32_t tO = 384;                            // stored while PV(j - 1) runs
+};
+
+struct Bars2sm {
+  uint64_t q_full;
+  uint64_t kv_full[8], kv_empty[8];
+  uint64_t s_full[2], s_free[2], p_full[2], pv_done[2];
+  uint32_t tmem_base;
 };
 
 template <int kPolyPer8>
@@ -744,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int seg = a.tiles[2 * blockIdx.y], tile0 = 2 * a.tiles[2 * blockIdx.y + 1];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  Bars1h* bars = reinterpret_cast<Bars1h*>(smem + C::kOffBar);
+  Bars2sm* bars = reinterpret_cast<Bars2sm*>(smem + C::kOffBar);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -763,8 +771,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     mbar_init(&bars->q_full, 1);
     for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
     for (int b = 0; b < 2; ++b) mbar_init(&bars->s_full[b], 1), mbar_init(&bars->s_free[b], kArrivals);
-    mbar_init(&bars->p_full, kArrivals);
-    mbar_init(&bars->pv_done, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&bars->p_full[b], kArrivals), mbar_init(&bars->pv_done[b], 1);
     fence_mbar_init();
   }
   if (warp == kMma) tmem_alloc_pair<512>(&bars->tmem_base);
@@ -831,13 +838,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         if (j > 0) {
           const int jv = j - 1;
           mbar_wait_sleep(&bars->kv_full[vunit(jv)], ((2 * jv + 1) / C::kUnits) & 1);
-          mbar_wait_sleep(&bars->p_full, jv & 1);
+          mbar_wait_sleep(&bars->p_full[jv & 1], (jv >> 1) & 1);
           tc_fence_after();
           const uint64_t dv = dv0 + ((uint32_t)(vunit(jv) * C::kKVBytes) >> 4);
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            umma2_f16_ts(tmem + C::tO, tmem + C::tP + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, jv > 0 || k > 0);
-          umma2_commit_both(&bars->pv_done);
+            umma2_f16_ts(tmem + C::tO, tmem + C::tP(jv & 1) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o,
+                         jv > 0 || k > 0);
+          umma2_commit_both(&bars->pv_done[jv & 1]);
           umma2_commit_both(&bars->kv_empty[vunit(jv)]);
         }
       }
@@ -848,9 +856,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     const int row = (warp % 4) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
     const uint32_t tO = tmem + lane_base + C::tO + w * (D / 2);
-    const uint32_t tP = tmem + lane_base + C::tP + w * (HN / 2);
+    const uint32_t tP0 = tmem + lane_base + C::tP(0) + w * (HN / 2);
     const uint32_t s_free_l[2] = {mapa_shared(&bars->s_free[0], 0), mapa_shared(&bars->s_free[1], 0)};
-    const uint32_t p_full_l = mapa_shared(&bars->p_full, 0);
+    const uint32_t p_full_l[2] = {mapa_shared(&bars->p_full[0], 0), mapa_shared(&bars->p_full[1], 0)};
     const uint32_t red = smem_u32(smem + C::kOffRed);                 // [parity][2][BM] maxima, [2][BM] sums
     const int qp = qp0 + row;
     const float sl2 = a.scale * 1.4426950408889634f;
@@ -913,10 +921,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
       }
-      if (j > 0) {
-        mbar_wait(&bars->pv_done, (j - 1) & 1);
-        tc_fence_after();
-      }
+      // P buffer j & 1 is free once PV(j - 2) has read it; O may be rescaled only once PV(j - 1)
+      // has accumulated into it (rare: lazy rescale)
+      if (j >= 2) mbar_wait(&bars->pv_done[b], ((j - 2) >> 1) & 1);
+      if (rescale && j > 0) mbar_wait(&bars->pv_done[b ^ 1], ((j - 1) >> 1) & 1);
+      tc_fence_after();
       if (rescale && j > 0) {
 #pragma unroll
         for (int c = 0; c < D / 2; c += 16) {
@@ -933,17 +942,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         }
       }
       l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y));
-      tmem_st32(tP, pk);
+      tmem_st32(tP0 + b * 64, pk);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full_l);
+      if (lane == 0) mbar_arrive_cluster(p_full_l[b]);
     }
     const uint32_t lsum = red + 4 * (2 * 2 * BM);
     st_shared_f32(lsum + 4 * (w * BM + row), l);
     named_bar_sync(1, kSm);
     l += ld_shared_f32(lsum + 4 * ((1 - w) * BM + row));
-    mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
+    mbar_wait(&bars->pv_done[(n_kv - 1) & 1], ((n_kv - 1) >> 1) & 1);
     tc_fence_after();
     const float inv_l = 1.f / l;
 #pragma unroll
