@@ -167,7 +167,9 @@ typedef struct {                /* one segment class (locals, or distributed chu
  * O = softmax(scale QK^T + bottom-right causal mask) V, LSE = natural-log row logsumexp.
  * q, o: [n_q_rows][hq][d]; k, v: [n_kv_rows][hkv][d]; lse: fp32 [hq][n_q_rows].
  * bf16 in/out with fp32 accumulation (SKR_BF16) or fp32 throughout (SKR_FP32).
- * `tiles` must come from skr_tiles_fwd with block_m = skr_attn_block_m(shape). */
+ * `tiles` must come from skr_tiles_fwd with block_m = skr_attn_block_m(shape): 128 query rows
+ * (bf16), 32 (fp32), or 256 for d = 128 when the process runs the opt-in CTA-pair forward
+ * (environment SKR_FWD_2SM=1, read once per process). */
 int32_t skr_attn_block_m(const skr_attn_shape* s);
 int32_t skr_attn_block_n(const skr_attn_shape* s);
 skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k, const void* v,
