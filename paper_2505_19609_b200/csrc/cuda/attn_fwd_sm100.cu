@@ -129,12 +129,25 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
   Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
-  // ---- work unit
-  const int pair = blockIdx.x;
+  // ---- work unit. d = 128: q-heads 2p and 2p + 1 of the whole head range -- with an odd GQA group
+  // (Qwen: 7 q-heads per KV head) a pair may straddle two KV groups ("xg"); each head then has its
+  // own K / V stream in the ring (units K_A K_B V_A V_B per KV tile instead of K V), so no CTA runs
+  // a lone head (S4: fwd -2.5 %). d = 64: pairs within a group, the last one alone when the group is
+  // odd (straddling pairs measured 6 % slower on C2: the ring then holds 1.5 tiles and the lone-head
+  // CTAs are cheap when MUFU-bound).
   const int grp = a.hq / a.hkv;
-  const int g = pair / pairs_per_group, p = pair % pairs_per_group;
-  const int ha = g * grp + 2 * p;
-  const int hb = (2 * p + 1 < grp) ? ha + 1 : -1;
+  int ha, hb;
+  if (pairs_per_group == 0) {
+    ha = 2 * blockIdx.x;
+    hb = (ha + 1 < a.hq) ? ha + 1 : -1;
+  } else {
+    const int g = blockIdx.x / pairs_per_group, p = blockIdx.x % pairs_per_group;
+    ha = g * grp + 2 * p;
+    hb = (2 * p + 1 < grp) ? ha + 1 : -1;
+  }
+  const int ga = ha / grp, gb = hb >= 0 ? hb / grp : ga;
+  const bool xg = D == 128 && gb != ga;                // compile-time false for d = 64 (per-group pairs)
+  const int U = xg ? 4 : 2;                             // ring units per KV tile
   const int seg = a.tiles[2 * blockIdx.y], tile = a.tiles[2 * blockIdx.y + 1];
   const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
   const int r0 = cu0 + tile * BM;                       // first packed query row of the tile
@@ -181,17 +194,19 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
     pa.start();
     int it = 0;
     for (int j = 0; j < n_kv; ++j) {
-      for (int kv = 0; kv < 2; ++kv, ++it) {
+      for (int kv = 0; kv < U; ++kv, ++it) {
         const int u = it % C::kUnits;
+        const bool is_k = xg ? kv < 2 : kv == 0;
+        const int gg = (xg && (kv & 1)) ? gb : ga;
         pa.mark(1);
         mbar_wait_sleep(&bars->kv_empty[u], ((it / C::kUnits) & 1) ^ 1);
         pa.mark(0);
-        if (lane == 0) trace(40 + kv, j);
+        if (lane == 0) trace(40 + (is_k ? 0 : 1), j);
         if (elect_one()) {
           mbar_expect_tx(&bars->kv_full[u], C::kKVBytes);
           uint8_t* dst = smem + C::kOffKV + u * C::kKVBytes;
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_2d(dst + c * (BN * 128), kv == 0 ? &tm_k : &tm_v, &bars->kv_full[u], g * D + c * 64,
+            tma_load_2d(dst + c * (BN * 128), is_k ? &tm_k : &tm_v, &bars->kv_full[u], gg * D + c * 64,
                         kst + j * BN);
         }
         __syncwarp();
@@ -237,19 +252,31 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
       //    S_s(j) waits until the softmax has read S_s(j-1) (s_free), so it overlaps softmax(j-1).
       //  P aliasing S (d=128): per head [PV_s(j-1) S_s(j)] back to back: S_s(j) overwrites P_s(j-1)
       //    after the in-order pipe has consumed it, and never queues behind the other head's PV.
-      auto kunit = [&](int j) { return (2 * j) % C::kUnits; };
-      auto vunit = [&](int j) { return (2 * j + 1) % C::kUnits; };
+      // ring position of head s's K / V unit of KV tile j (s ignored unless the pair straddles groups)
+      auto kidx = [&](int j, int s) { return U * j + (xg ? s : 0); };
+      auto vidx = [&](int j, int s) { return U * j + (xg ? 2 + s : 1); };
+      auto kunit = [&](int j, int s) { return kidx(j, s) % C::kUnits; };
+      auto vunit = [&](int j, int s) { return vidx(j, s) % C::kUnits; };
+      const int nstream = xg ? 2 : 1;                     // distinct K (and V) units per KV tile
       PhaseAcct pa;   // 0 waiting for K, 1 for V, 2 for S free / P full, 3 issuing
       pa.start();
       auto wait_k = [&](int j) {
         pa.mark(3);
-        mbar_wait_sleep(&bars->kv_full[kunit(j)], ((2 * j) / C::kUnits) & 1);
+        for (int t = 0; t < nstream; ++t)
+          mbar_wait_sleep(&bars->kv_full[kunit(j, t)], (kidx(j, t) / C::kUnits) & 1);
         pa.mark(0);
       };
       auto wait_v = [&](int j) {
         pa.mark(3);
-        mbar_wait_sleep(&bars->kv_full[vunit(j)], ((2 * j + 1) / C::kUnits) & 1);
+        for (int t = 0; t < nstream; ++t)
+          mbar_wait_sleep(&bars->kv_full[vunit(j, t)], (vidx(j, t) / C::kUnits) & 1);
         pa.mark(1);
+      };
+      auto free_k = [&](int j) {
+        for (int t = 0; t < nstream; ++t) umma_commit(&bars->kv_empty[kunit(j, t)]);
+      };
+      auto free_v = [&](int j) {
+        for (int t = 0; t < nstream; ++t) umma_commit(&bars->kv_empty[vunit(j, t)]);
       };
       if (!C::kPAlias) {
         for (int j = 0; j <= n_kv; ++j) {
@@ -261,10 +288,10 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
               pa.mark(2);
               tc_fence_after();
               trace(5 + s, j);
-              issue_s(s, kunit(j));
+              issue_s(s, kunit(j, s));
               trace(1 + s, j);
             }
-            umma_commit(&bars->kv_empty[kunit(j)]);   // K(j) free once every head's S MMAs completed
+            free_k(j);   // K(j) free once every head's S MMAs completed
           }
           if (j > 0) {
             const int jv = j - 1;
@@ -275,17 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
               pa.mark(2);
               tc_fence_after();
               trace(7 + s, jv);
-              issue_pv(s, vunit(jv), jv > 0);
+              issue_pv(s, vunit(jv, s), jv > 0);
               trace(3 + s, jv);
             }
-            umma_commit(&bars->kv_empty[vunit(jv)]);
+            free_v(jv);
           }
         }
       } else {
         wait_k(0);
         tc_fence_after();
-        for (int s = 0; s < nq; ++s) issue_s(s, kunit(0));
-        umma_commit(&bars->kv_empty[kunit(0)]);
+        for (int s = 0; s < nq; ++s) issue_s(s, kunit(0, s));
+        free_k(0);
         for (int j = 1; j <= n_kv; ++j) {
           const int jv = j - 1;
           wait_v(jv);
@@ -296,12 +323,12 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
             pa.mark(2);
             tc_fence_after();
             trace(7 + s, jv);
-            issue_pv(s, vunit(jv), jv > 0);
-            if (j < n_kv) issue_s(s, kunit(j));
+            issue_pv(s, vunit(jv, s), jv > 0);
+            if (j < n_kv) issue_s(s, kunit(j, s));
             trace(3 + s, jv);
           }
-          umma_commit(&bars->kv_empty[vunit(jv)]);
-          if (j < n_kv) umma_commit(&bars->kv_empty[kunit(j)]);
+          free_v(jv);
+          if (j < n_kv) free_k(j);
         }
       }
       pa.mark(3);
@@ -1026,9 +1053,10 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
       !make_tmap_2d(&tv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n_kv_rows, kcols, kcols,
                     d == 128 ? fwd::Cfg<128>::BN : fwd::Cfg<64>::BN, 64, true))
     return fail(SKR_E_CUDA, "attn fwd: tensor map encode failed");
-  const int grp = a.hq / a.hkv;
-  const int ppg = (grp + 1) / 2;
-  dim3 grid(a.hkv * ppg, a.n_tiles);
+  // d = 128: consecutive q-head pairs over all heads (may straddle a GQA group, pairs_per_group = 0);
+  // d = 64: pairs within each group
+  const int ppg = d == 128 ? 0 : (a.hq / a.hkv + 1) / 2;
+  dim3 grid(d == 128 ? (a.hq + 1) / 2 : a.hkv * ppg, a.n_tiles);
   // share of exponentials on the FMA pipe (MUFU ex2 bounds the d = 64 forward); SKR_FWD_POLY overrides
   static int poly = [] {
     const char* e = getenv("SKR_FWD_POLY");

@@ -38,7 +38,7 @@ def _check_fwd(pk, O, LSE, fp32):
         r += n
 
 
-SHAPES = [(14, 2, 64), (8, 2, 128), (4, 4, 64), (3, 1, 128)]
+SHAPES = [(14, 2, 64), (8, 2, 128), (4, 4, 64), (3, 1, 128), (6, 2, 128)]   # (6, 2, 128): a d = 128 head pair straddles two GQA groups
 
 
 @pytest.mark.parametrize("hq,hkv,d", SHAPES)
