@@ -86,6 +86,16 @@ def build(jobs: int = 8, verbose: bool = False, clean: bool = False) -> str:
         raise RuntimeError("nccl.h not found (pip nvidia-nccl); the CP collectives need it")
     cus, ccs, hdrs = _sources()
     hdr_mtime = max((os.path.getmtime(h) for h in hdrs), default=0)
+    # objects are reused only if they were compiled with the same flags (the trace / phase /
+    # variant modes share build dirs by name): a flag change rebuilds everything
+    stamp = os.path.join(BUILD, "flags.stamp")
+    sig = repr((cu_flags, cc_flags))
+    if not os.path.exists(stamp) or open(stamp).read() != sig:
+        for f in os.listdir(BUILD):
+            if f.endswith(".o"):
+                os.remove(os.path.join(BUILD, f))
+        with open(stamp, "w") as f:
+            f.write(sig)
     jobs_list = []
     objs = []
     for src in cus + ccs:
