@@ -1,12 +1,13 @@
 // Row a7: packed varlen causal attention forward on sm_100a (tcgen05 + TMEM + TMA).
 //
 // Work unit (CTA): one 128-row query tile of one segment x two q-heads of the same KV group
-// (GQA, R30), so each K/V tile is loaded once into shared memory and feeds both heads.
+// (GQA, R30), so each K/V tile is loaded once into shared memory and feeds both heads (d = 128 with
+// an odd group: one pair in each straddles two groups and streams both groups' K/V, see the kernel).
 // Warp roles (576 threads):
 //   warps 0-7  softmax of head A (ha): two warpgroups split the 128 key columns of each S tile
 //              (warpgroup 0 keys [0,64), warpgroup 1 keys [64,128)); thread = query row of the tile,
 //              the two halves of a row combine their maxima through shared memory once per tile
-//   warps 8-15 softmax of head B (hb = ha + 1, if it exists in the group), same split
+//   warps 8-15 softmax of head B (hb = ha + 1, if it exists), same split
 //   warp 16    TMA producer: Q tiles once, then a ring of K/V tiles (SW128, 64-col boxes)
 //   warp 17    MMA issuer (one thread): S = Q K^T into TMEM, O += P V into TMEM; S(j+1) is issued as
 //              soon as the softmax has read S(j) (s_free), overlapping the exponentials of tile j
