@@ -14,10 +14,24 @@ Metric (BASELINE.json): useful causal attention TFLOP/s fwd+bwd = sum_seq 14*d*H
 divided by the step time (max over ranks), whole-job aggregate. Inputs (Q, K, V, dO of the batch
 plus activations) exceed the 126 MB L2, so no explicit flush is done between steps.
 
+Workload (the same at every N, so BENCH and SCALE share it): S4n{N} -- BASELINE configs[3]'s
+global batch (Qwen2.5-7B attention shape 28/4, d=128; 511 `short1k` sequences + one 128K) with
+the SURVEY §8(d) strong-scaling BucketSize of that CP degree (512K / 96K / 48K / 24K tokens per
+rank at N = 1 / 2 / 4 / 8, so DACP shards the 128K sequence for N >= 2 and the plan floor stays
+<= 1.001). `--config NAME` selects another (C2 = configs[1] weak-scaled by N; C5n*/C5Hn* =
+configs[4]; C3n*, C4).
+
 Rank 0 prints ONE JSON line. Under torchrun (N>1) the ranks form a DP x CP grid (--dp, default 1:
 one CP group of N ranks; row f4): CP groups are blocks of N/dp consecutive ranks, GDS/LPT bins the
-batch over the DP ranks and DACP places inside each CP group. The workload is weak-scaled: N x the
-N=1 batch, C per rank fixed.
+batch over the DP ranks and DACP places inside each CP group.
+
+Timing: W untimed steps; then K steps between a barrier + synchronize on
+both sides. Before every step the ranks align their device timelines with a 1-element all-reduce
+on the main stream, and each step is bracketed by CUDA events; the library records 8 more events
+around its attention calls inside each composite step (skr_cp_step.timing_events), so the
+dominant kernel's time for the roofline comes from the SAME timed pass as the headline. Reported:
+the whole-loop time (max over ranks) as `ms_per_step`, the per-step max over ranks / mean over
+ranks with median and p10-p90, and the part of the step outside the attention calls.
 """
 from __future__ import annotations
 
@@ -58,26 +72,34 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- workload
+DEFAULT_WORKLOAD = "S4"   # S4n{cp}: configs[3]'s batch, strong-scaled over the CP group
+
+
 def workload(args, world):
-    """Global batch lengths, shape, CP degree and BucketSize for this run."""
-    name = args.config or "C2"
-    cfg = CONFIGS[name]
+    """Global batch lengths, shape, CP degree and BucketSize for this run:
+    -> (name, cfg, lens, shape, cp, bucket, scaling). cp = world // dp (DP x CP grid)."""
+    dp = args.dp
+    if dp < 1 or world % dp:
+        raise SystemExit(f"--dp {dp} does not divide {world} ranks")
+    cp = world // dp
+    name = args.config or f"{DEFAULT_WORKLOAD}n{cp}"
     if name == "C2":
+        cfg = CONFIGS[name]
         # weak scaling of configs[1]: N x (63 long-tail + one 32K) sequences over the DP x CP grid.
         # With CP >= 2 the BucketSize is set below the longest sequence (R33) so DACP shards it:
         # 30720 gives 3 micro-batches per rank with only the 32K sequences sharded at N = 8 and plan
         # floors 1.006 / 1.070 / 1.088 at N = 2 / 4 / 8 (24576: 4 / 4 / 3 micro-batches, 19 sequences
         # sharded at N = 8, floors 1.008 / 1.074 / 1.088).
-        cp = world // args.dp
         lens = np.concatenate([cfg.lengths(args.seed + r) for r in range(world)])
         bucket = cfg.bucket if cp == 1 else 30720
-        return name, cfg, np.asarray(lens, np.int64), cfg.shape, cp, bucket
-    else:
-        lens = cfg.lengths(args.seed)
-        bucket = cfg.bucket
-        if cfg.cp * args.dp != world:
-            raise SystemExit(f"config {name} is for CP={cfg.cp} x DP={args.dp}, launched with {world} ranks")
-    return name, cfg, np.asarray(lens, np.int64), cfg.shape, world, bucket
+        return name, cfg, np.asarray(lens, np.int64), cfg.shape, cp, bucket, "weak"
+    if name not in CONFIGS:
+        raise SystemExit(f"unknown config {name}; one of {sorted(CONFIGS)}")
+    cfg = CONFIGS[name]
+    if cfg.cp != cp:
+        raise SystemExit(f"config {name} is for CP={cfg.cp}; {world} ranks with --dp {dp} give CP={cp}")
+    scaling = "strong" if name.startswith("S4") else "weak"
+    return name, cfg, np.asarray(cfg.lengths(args.seed), np.int64), cfg.shape, cp, cfg.bucket, scaling
 
 
 def useful_flops(lens, shape: Shape, part="fwdbwd"):
@@ -194,7 +216,7 @@ def eval_prediction(sk, all_mbs, cp, bucket, shp):
 def cpu_oracle_sample(lens, shape: Shape, seconds: float, seed: int = 0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: sequences taken
     shortest-first while the projected time (measured FLOP rate so far x the next sequence's useful
-    FLOPs) stays within `seconds`. Returns (TFLOP/s, n_seqs, tokens, wall_s)."""
+    FLOPs) stays within `seconds`. Returns (TFLOP/s, n_seqs, tokens, wall_s, useful_flops)."""
     from oracle.attention import attn_bwd, attn_fwd
     from synth import seq_tensors
     order = np.argsort(lens, kind="stable")
@@ -212,7 +234,7 @@ def cpu_oracle_sample(lens, shape: Shape, seconds: float, seed: int = 0):
         done_flops += f
         n += 1
         toks += S
-    return done_flops / t_used / 1e12, n, toks, t_used
+    return done_flops / t_used / 1e12, n, toks, t_used, done_flops
 
 
 def run_reference(args):
@@ -220,24 +242,25 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
-    name, cfg, lens, shape, cp, bucket = workload(args, world)
+    name, cfg, lens, shape, cp, bucket, scaling = workload(args, world)
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    times, flops_done = [], 0
+    tot_flops, tot_t = 0, 0.0
     sample = None
     for i in range(args.warmup + args.steps):
-        v, n, toks, t = cpu_oracle_sample(lens, shape, per_step, args.seed)
+        v, n, toks, t, f = cpu_oracle_sample(lens, shape, per_step, args.seed)
         if i >= args.warmup:
-            times.append(t)
-            flops_done = v * t * 1e12
+            # the sample size is time-budgeted and may differ between iterations: sum the work
+            # and the time over the timed iterations (not the last iteration's work / mean time)
+            tot_flops += f
+            tot_t += t
             sample = f"{n} shortest sequences of the batch ({toks} tokens), fp64 naive attention fwd+bwd"
-    t = float(np.mean(times))
-    value = flops_done / t / 1e12
+    value = tot_flops / tot_t / 1e12
     cores = len(os.sched_getaffinity(0))
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+           "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": name, "shape": f"Hq={shape.hq} Hkv={shape.hkv} d={shape.d}", "cp": cp,
-                      "bucket": bucket, "global_batch": int(len(lens))},
+                      "bucket": int(bucket), "global_batch": int(len(lens))},
            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -245,6 +268,21 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU leg
+def pick_peak(peaks, clocks, timed_s):
+    """Roofline denominator: the measured BURST bf16 GEMM rate, unless the timed region ran for
+    seconds at power-capped clocks (median SM clock under load < 90 % of max), where the SUSTAINED
+    figure of the same measurement applies (B200_PROFILING.md)."""
+    burst = float(peaks.get("bf16_tflops", 1590.0))
+    sus = float(peaks.get("bf16_tflops_sustained", burst))
+    mhz, mx = clocks.get("sm_mhz"), clocks.get("sm_max_mhz")
+    sustained = bool(timed_s >= 2.0 and mhz and mx and mhz < 0.9 * mx)
+    return (sus, "bf16_tflops_sustained") if sustained else (burst, "bf16_tflops"), burst, sus
+
+
+def pctl(x, q):
+    return float(np.percentile(np.asarray(x, np.float64), q))
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -268,12 +306,13 @@ def run_ours(args):
     from paper_2505_19609_b200.runtime import BufferPool, RankStep, dp_micro_batches, grid_coords
 
     dp = args.dp
+    name, cfg, lens, shp, cp, bucket, scaling = workload(args, world)
     dp_rank, cp_rank, _ = grid_coords(rank, world, dp)
-    name, cfg, lens, shp, cp, bucket = workload(args, world)
     shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
     h, hkv = shp.hidden, shp.kv_hidden
 
-    # ---- a1-a4: host plan (every rank computes the identical plan)
+    # ---- a1-a4: host plan (every rank computes the identical plan); the Python scheduler
+    # oracle is timed beside it on rank 0 (the paper's "near-zero overhead")
     t0 = time.perf_counter()
     plan = sk.skr_plan(lens, bucket, cp, dp, h, hkv)
     plan_us = (time.perf_counter() - t0) * 1e6
@@ -289,7 +328,9 @@ def run_ours(args):
             comm = sk.PeerComm(cp, cp_rank, group=groups[dp_rank])
         else:
             comm = sk.Comm(cp, cp_rank, group=groups[dp_rank], src=dp_rank * cp)
+    nccl_comm = comm if (comm is not None and args.exchange != "peer") else None
     side = torch.cuda.Stream(priority=-1)
+    main = torch.cuda.current_stream()
     steps = []
     g = torch.Generator(device="cuda")
     # the micro-batches run one after another: their working buffers come from one shared pool
@@ -307,7 +348,7 @@ def run_ours(args):
                for k, hh in (("q", shp.hq), ("k", shp.hkv), ("v", shp.hkv), ("do", shp.hq))}
         steps.append((rs, src))
 
-    def fwd_bwd(rs, src, ev_do=None):
+    def fwd_bwd(rs, src, ev_do=None, timing=None):
         # ev_do (e2e only): the backward waits for this micro-batch's dO copy, the forward does not
         if args.exchange == "peer" and comm is not None:
             rs.forward_peer(src["q"], src["k"], src["v"], side)
@@ -315,14 +356,35 @@ def run_ours(args):
                 torch.cuda.current_stream().wait_event(ev_do)
             rs.backward_peer(src["do"], side)
         else:
-            rs.forward(src["q"], src["k"], src["v"], comm, side)
+            rs.forward(src["q"], src["k"], src["v"], comm, side, timing=timing)
             if ev_do is not None:
                 torch.cuda.current_stream().wait_event(ev_do)
-            rs.backward(src["do"], comm, side)
+            rs.backward(src["do"], comm, side, timing=timing)
 
-    def one_step():
-        for rs, src in steps:
-            fwd_bwd(rs, src)
+    def one_step(timing=None):
+        for j, (rs, src) in enumerate(steps):
+            fwd_bwd(rs, src, timing=timing[j] if timing is not None else None)
+
+    align_buf = torch.zeros(1, device="cuda")
+
+    def align():
+        # per-step alignment of the ranks' device timelines
+        if world > 1:
+            if backend == "nccl":
+                dist.all_reduce(align_buf)
+            else:
+                torch.cuda.synchronize()
+                dist.barrier()
+
+    def sync():
+        # comm-aware synchronize: an NCCL error or a dead peer surfaces as an exception after the
+        # timeout instead of a hang (skr_comm_wait polls ncclCommGetAsyncError); the peer exchange's
+        # timed-out waits are reported by PeerComm.check
+        if nccl_comm is not None:
+            nccl_comm.wait(main, timeout_s=600.0)
+        torch.cuda.synchronize()
+        if comm is not None and args.exchange == "peer":
+            comm.check()
 
     def barrier():
         if world > 1:
@@ -330,43 +392,61 @@ def run_ours(args):
 
     for _ in range(max(args.warmup, 0)):
         one_step()
-    torch.cuda.synchronize()
+    sync()
     barrier()
+
+    # per-(step, micro-batch) attention timing events (recorded by the library inside the composite
+    # steps); created up front so recording them costs nothing in the loop
+    K = args.steps
+    use_lib_timing = not (args.exchange == "peer" and comm is not None)
+    timing = None
+    if use_lib_timing:
+        timing = [[[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(n_mb)] for _ in range(K)]
+        for per_step in timing:
+            for evs in per_step:
+                for e in evs:
+                    e.record(main)
+    else:
+        for rs, _ in steps:
+            rs.events = []                     # the peer path's per-call events (fwd / bwd kinds)
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    sync()
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    sync()
     barrier()
     start.record()
-    for _ in range(args.steps):
-        one_step()
+    for i in range(K):
+        align()
+        ev_s[i].record(main)
+        one_step(timing[i] if timing is not None else None)
+        ev_e[i].record(main)
     end.record()
-    torch.cuda.synchronize()
+    sync()
     barrier()
     clocks = clk.stop()
-    my_ms = start.elapsed_time(end) / args.steps
-
-    # per-kernel timing pass (separate from the headline timing): CUDA events on the launching
-    # stream around every attention fwd / bwd C-ABI call
-    nrep = max(2, min(args.steps, 5))
-    for rs, _ in steps:
-        rs.events = []
-    for _ in range(nrep):
-        one_step()
-    torch.cuda.synchronize()
-    kt = {"fwd": 0.0, "bwd": 0.0}
-    for rs, _ in steps:
-        for kind, a, b in rs.events:
-            kt[kind] += a.elapsed_time(b)
-        rs.events = None
-    fwd_ms, bwd_ms = kt["fwd"] / nrep, kt["bwd"] / nrep
+    my_ms = start.elapsed_time(end) / K
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+    if timing is not None:
+        el = lambda evs, a, b: evs[a].elapsed_time(evs[b])  # noqa: E731
+        fwd_ms = sum(el(evs, 0, 1) + el(evs, 2, 3) for per in timing for evs in per) / K
+        bwd_ms = sum(el(evs, 4, 5) + el(evs, 6, 7) for per in timing for evs in per) / K
+    else:
+        kt = {"fwd": 0.0, "bwd": 0.0}
+        for rs, _ in steps:
+            for kind, a, b in rs.events:
+                kt[kind] += a.elapsed_time(b)
+            rs.events = None
+        fwd_ms, bwd_ms = kt["fwd"] / K, kt["bwd"] / K
 
     # ---- e2e: host pinned inputs -> device, step, gradients back to host. Pipelined like a
     # prefetching DataLoader: two device input sets; the H2D of step k+1 and the D2H of step k's
     # gradients (staged by a device copy) run on two copy streams (one per direction of the host link)
-    # while step k computes. Every timed
-    # step still moves all of its inputs in and all of its gradients out.
+    # while step k computes. Every timed step still moves all of its inputs in and all of its
+    # gradients out.
     e2e = None
     if not args.no_e2e:
         host = [{k: v.cpu().pin_memory() for k, v in src.items()} for _, src in steps]
@@ -379,10 +459,8 @@ def run_ours(args):
         # working buffers, so each micro-batch's gradients are staged right after its backward)
         stage = [[{k: torch.empty_like(o[k], device="cuda") for k in o} for o in outs] for _ in range(2)]
         copy, copy_out = torch.cuda.Stream(), torch.cuda.Stream()   # one per direction (full duplex)
-        main = torch.cuda.current_stream()
         # per input set and micro-batch: one event once its Q, K, V are in (the forward may start),
         # one once its dO is in (the backward may start)
-        n_mb = len(steps)
         ev_qkv = [[torch.cuda.Event() for _ in range(n_mb)] for _ in range(2)]
         ev_do = [[torch.cuda.Event() for _ in range(n_mb)] for _ in range(2)]
         ev_used = [torch.cuda.Event(), torch.cuda.Event()]
@@ -429,19 +507,20 @@ def run_ours(args):
             main.wait_event(ev_out_free[1])
 
         e2e_run(2)
-        torch.cuda.synchronize()
+        sync()
         barrier()
         s2, e2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record()
-        e2e_run(args.steps)
+        e2e_run(K)
         e2_.record()
-        torch.cuda.synchronize()
+        sync()
         barrier()
-        e2e_ms = s2.elapsed_time(e2_) / args.steps
+        e2e_ms = s2.elapsed_time(e2_) / K
         e2e = (e2e_ms, h2d, d2h)
 
-    # ---- reduce over ranks: max (headline), per-rank list (imbalance)
-    vals = torch.tensor([my_ms, fwd_ms, bwd_ms, e2e[0] if e2e else 0.0], device="cuda", dtype=torch.float64)
+    # ---- reduce over ranks: max (headline), per-rank lists (imbalance per step)
+    vals = torch.tensor([my_ms, fwd_ms, bwd_ms, e2e[0] if e2e else 0.0] + step_ms, device="cuda",
+                        dtype=torch.float64)
     if world > 1:
         if backend != "nccl":
             vals = vals.cpu()                 # gloo moves host tensors
@@ -450,27 +529,40 @@ def run_ours(args):
         allv = torch.stack(allv).cpu().numpy()
     else:
         allv = vals.cpu().numpy()[None]
-    step_ms = float(allv[:, 0].max())
+    loop_ms = float(allv[:, 0].max())
     total_flops = useful_flops(lens, shp)
-    value = total_flops / (step_ms * 1e-3) / 1e12
+    value = total_flops / (loop_ms * 1e-3) / 1e12
 
     if rank == 0:
+        per_step = allv[:, 4:]                                  # [ranks, K]
+        step_max, step_mean = per_step.max(axis=0), per_step.mean(axis=0)
+        imb = step_max / np.maximum(step_mean, 1e-12)
+        step_tflops = total_flops / (step_max * 1e-3) / 1e12
         peaks, which = measured_peaks()
-        # dominant kernel: forward or backward attention call of the local class at N=1
-        # (algorithmic flops of this rank: 4 / 10 * d * Hq per causal pair it computes)
+        (peak, peak_key), burst, sus = pick_peak(peaks, clocks, loop_ms * K / 1e3)
+        # dominant kernel: the forward or backward attention calls of rank 0 (algorithmic flops of
+        # this rank: 4 / 10 * d * Hq per causal pair it computes), timed inside the headline loop
         my_pairs = sum(rank_pairs(ml, ma, cp, cp_rank) for ml, ma in mbs)
         fwd_fl, bwd_fl = 4 * shp.d * shp.hq * my_pairs, 10 * shp.d * shp.hq * my_pairs
-        dom = ("bwd", bwd_fl, bwd_ms) if bwd_ms >= fwd_ms else ("fwd", fwd_fl, fwd_ms)
+        my_fwd, my_bwd = float(allv[0, 1]), float(allv[0, 2])
+        dom = ("bwd", bwd_fl, my_bwd) if my_bwd >= my_fwd else ("fwd", fwd_fl, my_fwd)
         achieved = dom[1] / (dom[2] * 1e-3) / 1e12
         traffic = ncu_traffic(name, world, dom[0])
-        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-        gpu_launches = args.steps * sum(rs.launches_per_step(args.exchange) for rs, _ in steps)
+        launches_per_step = sum(rs.launches_per_step(args.exchange) for rs, _ in steps)
+        gpu_launches = K * launches_per_step
         cpu = None
         if not args.no_cpu_baseline and world == 1:   # the oracle baseline is an N=1 figure
-            v, n, toks, t = cpu_oracle_sample(lens, shp, args.cpu_seconds, args.seed)
+            v, n, toks, t, _ = cpu_oracle_sample(lens, shp, args.cpu_seconds, args.seed)
             cpu = {"value": v, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"{n} shortest sequences ({toks} tokens) of the batch, fp64 numpy fwd+bwd, {t:.1f} s"}
-        mean_rank = float(allv[:, 0].mean())
+        # the Python scheduler oracle (exact Fractions, Alg. 1-3 + LPT) on the same global batch,
+        # beside the C++ skr_plan (SURVEY §8(d) "Oracle timing beside the GPU path")
+        from oracle.cost_model import Model
+        from oracle.schedule import plan as oracle_plan
+        t0 = time.perf_counter()
+        ref = oracle_plan([int(x) for x in lens], int(bucket), cp, dp, Model(h, hkv))
+        oracle_plan_us = (time.perf_counter() - t0) * 1e6
+        assert list(ref.assign) == list(plan["assign"]), "skr_plan differs from the scheduler oracle"
         # plan floor (Eq. 8 style): per DP rank, sum over its micro-batches of the slowest CP rank's
         # causal pairs; the slowest DP rank over the mean pairs per GPU
         t_dp, tot = [], 0
@@ -480,23 +572,28 @@ def run_ours(args):
             tot += sum(sum(p) for p in pp)
         floor = max(t_dp) / max(1e-9, tot / world)
         predicted = eval_prediction(sk, all_mbs, cp, bucket, shp)
+        attn_ms = my_fwd + my_bwd
         out = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": loop_ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": name, "desc": cfg.note if world == 1 else f"{cfg.note}; weak-scaled x{world}",
+            "config": {"workload": name, "desc": cfg.note if (world == 1 or name != "C2") else f"{cfg.note}; weak-scaled x{world}",
                        "shape": f"Hq={shp.hq} Hkv={shp.hkv} d={shp.d}", "global_batch": int(len(lens)),
                        "tokens": int(lens.sum()), "max_seq_len": int(lens.max()), "cp": cp, "dp": dp,
                        "bucket_tokens": int(bucket), "micro_batches": n_mb,
                        "distributed_seqs": int((plan["assign"] == -1).sum()),
                        "rollbacks": int(plan["n_rollbacks"]),
-                       "l2": "inputs larger than L2 (no flush)", "parallelism": f"dp{dp}xcp{cp}" if dp > 1 else f"cp{cp}",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"dp{dp}xcp{cp}" if dp > 1 else f"cp{cp}",
                        "exchange": args.exchange if cp > 1 else None},
-            "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]}", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak,
+            "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]} calls (rank 0, inside the timed loop; "
+                                                      f"bwd includes its D-preprocess and dQ convert)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "frac_of_burst": achieved / burst, "frac_of_sustained": achieved / sus,
                          "traffic": traffic[0] if traffic else None,
                          "traffic_source": traffic[1] if traffic else None,
-                         "peak_source": f"{which} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
+                         "peak_source": f"{which} {peak_key} (MEASURED_PEAKS.json); sustained applies when the "
+                                        f"timed region is >= 2 s at power-capped clocks"},
             "cpu_baseline": cpu,
             "e2e": None if e2e is None else {"value": total_flops / (float(allv[:, 3].max()) * 1e-3) / 1e12,
                                              "unit": "TFLOP/s", "h2d_bytes_per_step": e2e[1],
@@ -504,11 +601,17 @@ def run_ours(args):
                                              "pipeline": "H2D of step k+1 and D2H of step k overlap step k"},
             "gpu_launches": gpu_launches,
             "clocks": clocks,
-            "max_mean_rank_time": step_ms / mean_rank,
+            "max_mean_rank_time": float(np.median(imb)),
+            "max_mean_rank_time_p10_p90": [pctl(imb, 10), pctl(imb, 90)],
+            "step_tflops_median": float(np.median(step_tflops)),
+            "step_tflops_p10_p90": [pctl(step_tflops, 10), pctl(step_tflops, 90)],
             "plan_floor": floor,
             "eval_predicted_ms": predicted,
-            "plan_us": plan_us,
+            "plan_us": plan_us, "plan_us_oracle_python": oracle_plan_us,
             "fwd_ms": float(allv[:, 1].max()), "bwd_ms": float(allv[:, 2].max()),
+            "rest_of_step_ms": loop_ms - attn_ms,
+            "rest_of_step": "pack Q/K/V/dO, K/V exchange waits, dK/dV partial zeroing, launch gaps and the "
+                            "per-step rank alignment (rank 0)",
         }
         print(json.dumps(out), flush=True)
     if comm:

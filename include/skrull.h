@@ -168,8 +168,8 @@ typedef struct {                /* one segment class (locals, or distributed chu
  * q, o: [n_q_rows][hq][d]; k, v: [n_kv_rows][hkv][d]; lse: fp32 [hq][n_q_rows].
  * bf16 in/out with fp32 accumulation (SKR_BF16) or fp32 throughout (SKR_FP32).
  * `tiles` must come from skr_tiles_fwd with block_m = skr_attn_block_m(shape): 128 query rows
- * (bf16), 32 (fp32), or 256 for d = 128 when the process runs the opt-in CTA-pair forward
- * (environment SKR_FWD_2SM=1, read once per process). */
+ * (bf16), 32 (fp32), or 256 for d = 128 in the CTA-pair forward variant library
+ * (libskrull_fwd2sm.so, built with -DSKR_FWD_2SM_BUILD; fixed per library build, never switched at run time). */
 int32_t skr_attn_block_m(const skr_attn_shape* s);
 int32_t skr_attn_block_n(const skr_attn_shape* s);
 skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k, const void* v,
@@ -196,7 +196,9 @@ skr_status skr_unpack_rows(const void* src, const int32_t* src_row, int32_t n_ro
 /* a6 reorder: gathered [N][P] rank-major rows -> natural distributed order, via the chunk table. */
 skr_status skr_gather_chunks(const void* gathered, const int32_t* chunk_table, int32_t n_chunks, int32_t row_bytes,
                              void* natural, void* stream);
-/* a9 permute: natural fp32 partials -> rank-major [N][P] rows (rows beyond a rank's count zeroed). */
+/* a9 permute: natural fp32 partials -> rank-major [N][P] rows. chunk_table must be skr_pack_chunks'
+ * (2N rows per distributed sequence, else SKR_E_ARG); the same launch zeroes exactly the padding
+ * rows of each rank slot (beyond the rank's own distributed rows: the reduce-scatter sums them). */
 skr_status skr_scatter_chunks(const void* natural, const int32_t* chunk_table, int32_t n_chunks, int32_t row_bytes,
                               int32_t pad_rows_P, int32_t cp, void* rankmajor, void* stream);
 /* a9 cast: fp32 -> bf16, n elements. */
@@ -229,7 +231,8 @@ skr_status skr_peer_reduce_chunks(const uint64_t* peer_partials, int32_t nranks,
 /* Epoch flags (uint32 per rank): signal stores `epoch` into slot `rank` of every peer's flag array
  * (system-scope release after a system fence, ordered after this stream's earlier work); wait
  * blocks the stream until every slot of this rank's flags reached `epoch`, or sets *err = 1 after
- * ~10 s (a peer never signalled) instead of hanging. */
+ * ~10 s (a peer never signalled) instead of hanging; the stream then continues on stale peer data,
+ * so the caller must read *err after synchronising (and clear it) before trusting the step. */
 skr_status skr_peer_signal(const uint64_t* peer_flags, int32_t nranks, int32_t rank, uint32_t epoch, void* stream);
 skr_status skr_peer_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, int32_t* err, void* stream);
 
@@ -243,6 +246,16 @@ skr_status skr_comm_all_gather(skr_comm* c, const void* send, void* recv, size_t
 skr_status skr_comm_reduce_scatter_f32(skr_comm* c, const float* send, float* recv, size_t count_per_rank,
                                        void* stream);
 skr_status skr_comm_all_reduce_f32(skr_comm* c, float* buf, size_t count, void* stream);
+/* Size and this rank's index of the communicator. */
+skr_status skr_comm_size(const skr_comm* c, int32_t* nranks, int32_t* rank);
+/* SKR_E_NCCL if the communicator reported an asynchronous error (ncclCommGetAsyncError) or was aborted. */
+skr_status skr_comm_async_error(skr_comm* c);
+/* Failure detection: block the HOST until the work enqueued on `stream` so far has
+ * finished, polling the communicator's asynchronous error state; on an NCCL error, or if the work is
+ * not done after timeout_s seconds (a dead or stalled peer), abort the communicator (releasing NCCL
+ * kernels blocked on the peer) and return SKR_E_NCCL. An aborted communicator rejects further use;
+ * skr_comm_destroy still frees it. */
+skr_status skr_comm_wait(skr_comm* c, void* stream, double timeout_s);
 
 /* ------------------------------------------------------------------ a5-a9 as one call per direction
  * The CP-rank step of one micro-batch (Eq. 2, mirrored for the
@@ -282,6 +295,12 @@ typedef struct {
   float *dk_reduced, *dv_reduced;                 /* [P][hkv][d] fp32 (reduce-scatter output) */
   void* ws;                                       /* skr_attn_bwd workspace for buf_rows */
   size_t ws_bytes;
+  void* const* timing_events;   /* optional (NULL: none): 8 caller-created cudaEvent_t recorded on
+                                   the main stream around the attention calls (row a10 per-kernel
+                                   timing inside the step): fwd [0] before / [1] after the LOCAL
+                                   call, [2] before (after the exchange wait) / [3] after the
+                                   DISTRIBUTED call; bwd [4] / [5] DISTRIBUTED, [6] / [7] LOCAL. The
+                                   events of a call that is skipped are recorded back to back. */
 } skr_cp_step;
 skr_status skr_cp_attn_fwd(skr_comm* comm, const skr_attn_plan* plan, const skr_cp_step* step, void* main_stream,
                            void* side_stream);

@@ -27,6 +27,11 @@ _VARIANT = os.environ.get("SKR_VARIANT", "")
 _SUFFIX = "_trace" if _TRACE else (f"_{_VARIANT}" if _VARIANT else "")
 BUILD = os.path.join(ROOT, "build" + _SUFFIX)
 LIB = os.path.join(PKG, f"libskrull{_SUFFIX}.so")
+# Shipped build variants (built by __graft_entry__.build() next to the production library; a
+# variant is selected per process with SKR_LIB_PATH, never by switching a library at run time):
+#   fwd2sm: the d = 128 forward on CTA pairs (cta_group::2, 256-row super tiles; skr_attn_block_m
+#           answers 256 for d = 128 in this library only)
+VARIANTS = {"fwd2sm": ["-DSKR_FWD_2SM_BUILD"]}
 INCLUDE = os.path.join(ROOT, "include")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
@@ -44,7 +49,8 @@ def _nccl_dir():
     return None
 
 
-def _flags():
+def _flags(lib=None, defs=None):
+    lib = lib or LIB
     nccl = _nccl_dir()
     inc = ["-I", INCLUDE, "-I", CSRC]
     if nccl:
@@ -54,13 +60,15 @@ def _flags():
         trace.append("-DSKR_PHASE_ACCT" if os.environ["SKR_KERNEL_TRACE"] == "phase" else "-DSKR_KERNEL_TRACE")
     if _TRACE and os.environ.get("SKR_TRACE_SOFTMAX"):
         trace.append("-DSKR_TRACE_SOFTMAX")
-    if _VARIANT:
+    if defs is not None:
+        trace += list(defs)
+    elif _VARIANT:
         trace += os.environ.get("SKR_VARIANT_DEFS", "").split()
     cu = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", *trace,
           "--expt-relaxed-constexpr", "-Xptxas", "-v", *inc]
     cc = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
           "-Wno-unused-parameter", "-I", os.path.join(CUDA, "include"), *inc]
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, "-Xlinker", "--no-undefined"]
+    link = [NVCC, *ARCH, "-shared", "-o", lib, "-Xlinker", "--no-undefined"]
     libs = ["-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     if nccl:
         libs += ["-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
@@ -77,30 +85,37 @@ def _sources():
     return cus, ccs, hdrs
 
 
-def build(jobs: int = 8, verbose: bool = False, clean: bool = False) -> str:
-    if clean and os.path.isdir(BUILD):
-        shutil.rmtree(BUILD)
-    os.makedirs(BUILD, exist_ok=True)
-    cu_flags, cc_flags, link, libs, have_nccl = _flags()
+def build(jobs: int = 8, verbose: bool = False, clean: bool = False, variant: str | None = None) -> str:
+    """Build the production library (variant None; the SKR_VARIANT / SKR_KERNEL_TRACE experiment
+    environment applies) or one of the shipped VARIANTS. Returns the library path."""
+    if variant is not None:
+        BUILD_, LIB_ = os.path.join(ROOT, "build_" + variant), os.path.join(PKG, f"libskrull_{variant}.so")
+        defs = VARIANTS[variant]
+    else:
+        BUILD_, LIB_, defs = BUILD, LIB, None
+    if clean and os.path.isdir(BUILD_):
+        shutil.rmtree(BUILD_)
+    os.makedirs(BUILD_, exist_ok=True)
+    cu_flags, cc_flags, link, libs, have_nccl = _flags(LIB_, defs)
     if not have_nccl:
         raise RuntimeError("nccl.h not found (pip nvidia-nccl); the CP collectives need it")
     cus, ccs, hdrs = _sources()
     hdr_mtime = max((os.path.getmtime(h) for h in hdrs), default=0)
     # objects are reused only if they were compiled with the same flags (the trace / phase /
     # variant modes share build dirs by name): a flag change rebuilds everything
-    stamp = os.path.join(BUILD, "flags.stamp")
+    stamp = os.path.join(BUILD_, "flags.stamp")
     sig = repr((cu_flags, cc_flags))
     if not os.path.exists(stamp) or open(stamp).read() != sig:
-        for f in os.listdir(BUILD):
+        for f in os.listdir(BUILD_):
             if f.endswith(".o"):
-                os.remove(os.path.join(BUILD, f))
+                os.remove(os.path.join(BUILD_, f))
         with open(stamp, "w") as f:
             f.write(sig)
     jobs_list = []
     objs = []
     for src in cus + ccs:
         rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
-        obj = os.path.join(BUILD, rel + ".o")
+        obj = os.path.join(BUILD_, rel + ".o")
         objs.append(obj)
         if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
             continue
@@ -122,11 +137,11 @@ def build(jobs: int = 8, verbose: bool = False, clean: bool = False) -> str:
                 print(f"[build] {os.path.relpath(src, ROOT)}")
                 if err.strip():
                     print(err)
-    if jobs_list or not os.path.exists(LIB):
+    if jobs_list or not os.path.exists(LIB_):
         r = subprocess.run(link + objs + libs, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed\n{r.stderr}")
-    return LIB
+    return LIB_
 
 
 def main():
@@ -134,8 +149,9 @@ def main():
     ap.add_argument("--clean", action="store_true")
     ap.add_argument("-j", type=int, default=8)
     ap.add_argument("-v", action="store_true")
+    ap.add_argument("--variant", default=None, choices=sorted(VARIANTS))
     a = ap.parse_args()
-    print(build(a.j, a.v, a.clean))
+    print(build(a.j, a.v, a.clean, a.variant))
 
 
 if __name__ == "__main__":

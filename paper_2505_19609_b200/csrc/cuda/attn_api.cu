@@ -3,7 +3,7 @@
 #include "device.cuh"
 
 namespace skr {
-bool fwd_two_sm();   // attn_fwd_sm100.cu: d = 128 forward on CTA pairs (SKR_FWD_2SM=1)
+bool fwd_two_sm();   // attn_fwd_sm100.cu: d = 128 forward on CTA pairs (the libskrull_fwd2sm.so build variant)
 skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k, const void* v, void* o, float* lse,
                           int n_q_rows, int n_kv_rows, cudaStream_t st);
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,

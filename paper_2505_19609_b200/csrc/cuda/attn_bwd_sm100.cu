@@ -52,6 +52,11 @@ __device__ __forceinline__ void trace(int ev) {
 }
 
 constexpr int BN = 128;  // key tile
+// Grid order: 0 = (KV head, key tile) with the head fastest; 1 = (key tile, KV head), every key
+// tile of one KV head before the next, so the CTAs in flight share one group's Q / dO / dQ rows.
+#ifndef SKR_GRID_HEAD_MAJOR
+#define SKR_GRID_HEAD_MAJOR 0
+#endif
 constexpr int kThreads = 448;
 constexpr int kComputeThreads = 256;
 
@@ -145,8 +150,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* aux = reinterpret_cast<float*>(smem + C::kOffAux);  // lse2[kStages][BQ] then dd[kStages][BQ]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
-  const int g = blockIdx.x;
-  const int seg = a.tiles[2 * blockIdx.y], ktile = a.tiles[2 * blockIdx.y + 1];
+  const int g = SKR_GRID_HEAD_MAJOR ? blockIdx.y : blockIdx.x;
+  const int bt = SKR_GRID_HEAD_MAJOR ? blockIdx.x : blockIdx.y;
+  const int seg = a.tiles[2 * bt], ktile = a.tiles[2 * bt + 1];
   const int grp = a.hq / a.hkv;
   const int cu0 = a.cu[seg], q_len = a.cu[seg + 1] - cu0;
   const int q_pos = a.q_pos[seg], k_len = a.k_len[seg], kst = a.k_start[seg];
@@ -828,7 +834,7 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
         !make_tmap_2d(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n_q_rows, qcols, qcols,
                       d == 128 ? 32 : bq, 32, true))   // d = 128 reduces in 32-query halves
       return fail(SKR_E_CUDA, "attn bwd: tensor map encode failed");
-    dim3 grid(a.hkv, a.n_tiles);
+    dim3 grid = SKR_GRID_HEAD_MAJOR ? dim3(a.n_tiles, a.hkv) : dim3(a.hkv, a.n_tiles);
     // share of exponentials on the FMA pipe; SKR_BWD_POLY (0-3) overrides for sweeps
     static int poly = [] {
       const char* e = getenv("SKR_BWD_POLY");

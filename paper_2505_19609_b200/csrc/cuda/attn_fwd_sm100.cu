@@ -78,6 +78,14 @@ __device__ __forceinline__ void trace_smw(int, int) {}
 
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 576;
+// Grid order of the two-head kernel: 0 = (head pair, tile) with the pair fastest; 1 = (tile, head
+// pair), every tile of one pair before the next pair, so the CTAs in flight share one KV head's K / V
+// (L2-resident) instead of streaming every head's.
+#ifndef SKR_GRID_HEAD_MAJOR
+#define SKR_GRID_HEAD_MAJOR 0
+#endif
+__device__ __forceinline__ int blk_pair() { return SKR_GRID_HEAD_MAJOR ? blockIdx.y : blockIdx.x; }
+__device__ __forceinline__ int blk_tile() { return SKR_GRID_HEAD_MAJOR ? blockIdx.x : blockIdx.y; }
 constexpr int kSoftmax = 256;                // threads per head (two warpgroups)
 constexpr int kTmaWarp = 16, kMmaWarp = 17;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -139,17 +147,17 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
   const int grp = a.hq / a.hkv;
   int ha, hb;
   if (pairs_per_group == 0) {
-    ha = 2 * blockIdx.x;
+    ha = 2 * blk_pair();
     hb = (ha + 1 < a.hq) ? ha + 1 : -1;
   } else {
-    const int g = blockIdx.x / pairs_per_group, p = blockIdx.x % pairs_per_group;
+    const int g = blk_pair() / pairs_per_group, p = blk_pair() % pairs_per_group;
     ha = g * grp + 2 * p;
     hb = (2 * p + 1 < grp) ? ha + 1 : -1;
   }
   const int ga = ha / grp, gb = hb >= 0 ? hb / grp : ga;
   const bool xg = D == 128 && gb != ga;                // compile-time false for d = 64 (per-group pairs)
   const int U = xg ? 4 : 2;                             // ring units per KV tile
-  const int seg = a.tiles[2 * blockIdx.y], tile = a.tiles[2 * blockIdx.y + 1];
+  const int seg = a.tiles[2 * blk_tile()], tile = a.tiles[2 * blk_tile() + 1];
   const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
   const int r0 = cu0 + tile * BM;                       // first packed query row of the tile
   const int n_valid = min(BM, cu1 - r0);
@@ -1034,12 +1042,14 @@ extern "C" __attribute__((visibility("default"))) int skr_debug_fwd_trace(unsign
   return n;
 }
 
+// The CTA-pair d = 128 forward is a build-time variant (libskrull_fwd2sm.so, -DSKR_FWD_2SM_BUILD):
+// skr_attn_block_m's answer is then fixed for the library, not switched by the environment.
 bool fwd_two_sm() {
-  static const bool on = [] {
-    const char* e = getenv("SKR_FWD_2SM");
-    return e && atoi(e) != 0;
-  }();
-  return on;
+#ifdef SKR_FWD_2SM_BUILD
+  return true;
+#else
+  return false;
+#endif
 }
 
 skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k, const void* v, void* o, float* lse,
@@ -1057,7 +1067,8 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   // d = 128: consecutive q-head pairs over all heads (may straddle a GQA group, pairs_per_group = 0);
   // d = 64: pairs within each group
   const int ppg = d == 128 ? 0 : (a.hq / a.hkv + 1) / 2;
-  dim3 grid(d == 128 ? (a.hq + 1) / 2 : a.hkv * ppg, a.n_tiles);
+  const int n_pairs = d == 128 ? (a.hq + 1) / 2 : a.hkv * ppg;
+  dim3 grid = SKR_GRID_HEAD_MAJOR ? dim3(a.n_tiles, n_pairs) : dim3(n_pairs, a.n_tiles);
   // share of exponentials on the FMA pipe (MUFU ex2 bounds the d = 64 forward); SKR_FWD_POLY overrides
   static int poly = [] {
     const char* e = getenv("SKR_FWD_POLY");

@@ -1,11 +1,20 @@
 // Rows a6 / a9: CP-group collectives over NVLink 5 / NVSwitch (NCCL inside the CP group only).
+// Failure detection: skr_comm_wait polls the communicator's asynchronous error state
+// while it waits for a stream, and aborts the communicator (which releases NCCL kernels stuck on a
+// dead peer) on an error or after a timeout, so a failed rank surfaces as SKR_E_NCCL instead of a
+// hung process.
 #include <nccl.h>
+
+#include <chrono>
+#include <thread>
 
 #include "device.cuh"
 
 struct skr_comm {
   ncclComm_t comm = nullptr;
   int nranks = 0, rank = 0;
+  bool aborted = false;
+  cudaEvent_t ev = nullptr;   // skr_comm_wait's marker (created on first use, on the caller's device)
 };
 
 namespace {
@@ -42,8 +51,52 @@ SKR_EXPORT skr_status skr_comm_create(const void* nccl_id, int32_t nranks, int32
 
 SKR_EXPORT void skr_comm_destroy(skr_comm* c) {
   if (!c) return;
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm && !c->aborted) ncclCommDestroy(c->comm);
+  if (c->ev) cudaEventDestroy(c->ev);
   delete c;
+}
+
+SKR_EXPORT skr_status skr_comm_size(const skr_comm* c, int32_t* nranks, int32_t* rank) {
+  SKR_REQUIRE(c && nranks && rank, "skr_comm_size: null argument");
+  *nranks = c->nranks;
+  *rank = c->rank;
+  return SKR_OK;
+}
+
+SKR_EXPORT skr_status skr_comm_async_error(skr_comm* c) {
+  SKR_REQUIRE(c && c->comm, "skr_comm_async_error: no communicator");
+  if (c->aborted) return skr::fail(SKR_E_NCCL, "communicator was aborted");
+  ncclResult_t r = ncclSuccess;
+  if (skr_status s = nccl_status(ncclCommGetAsyncError(c->comm, &r), "ncclCommGetAsyncError")) return s;
+  if (r != ncclSuccess && r != ncclInProgress) return skr::fail(SKR_E_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(r));
+  return SKR_OK;
+}
+
+SKR_EXPORT skr_status skr_comm_wait(skr_comm* c, void* stream, double timeout_s) {
+  SKR_REQUIRE(c && c->comm && timeout_s > 0, "skr_comm_wait: bad arguments");
+  if (c->aborted) return skr::fail(SKR_E_NCCL, "communicator was aborted");
+  if (!c->ev && cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess)
+    return skr::fail(SKR_E_CUDA, "skr_comm_wait: event create");
+  if (cudaEventRecord(c->ev, (cudaStream_t)stream) != cudaSuccess) return skr::fail(SKR_E_CUDA, "skr_comm_wait: record");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaEventQuery(c->ev);
+    if (q == cudaSuccess) return SKR_OK;
+    if (q != cudaErrorNotReady) return skr::fail(SKR_E_CUDA, "skr_comm_wait: %s", cudaGetErrorString(q));
+    ncclResult_t r = ncclSuccess;
+    ncclCommGetAsyncError(c->comm, &r);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((r != ncclSuccess && r != ncclInProgress) || el > timeout_s) {
+      ncclCommAbort(c->comm);   // unblocks NCCL kernels waiting on a dead peer
+      c->aborted = true;
+      if (r != ncclSuccess && r != ncclInProgress)
+        return skr::fail(SKR_E_NCCL, "rank %d: asynchronous NCCL error: %s (communicator aborted)", c->rank,
+                    ncclGetErrorString(r));
+      return skr::fail(SKR_E_NCCL, "rank %d: step not done after %.1f s (a peer is dead or stalled; communicator aborted)",
+                  c->rank, timeout_s);
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
 }
 
 SKR_EXPORT skr_status skr_comm_all_gather(skr_comm* c, const void* send, void* recv, size_t bytes_per_rank,

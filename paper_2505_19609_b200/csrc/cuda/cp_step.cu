@@ -25,16 +25,20 @@ struct skr_attn_plan {
 
 namespace {
 
-struct Events {   // per host thread: the two cross-stream hand-overs of a call
+struct Events {   // per host thread and device: the two cross-stream hand-overs of a call
   cudaEvent_t a = nullptr, b = nullptr;
-  Events() {
-    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
-  }
 };
+// events belong to the device that was current when they were created: keyed by device ordinal
 Events& events() {
-  thread_local Events ev;
-  return ev;
+  thread_local Events ev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Events& e = ev[(dev >= 0 && dev < 64) ? dev : 0];
+  if (!e.a) {
+    cudaEventCreateWithFlags(&e.a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e.b, cudaEventDisableTiming);
+  }
+  return e;
 }
 
 skr_status check_step(const skr_attn_plan* plan, const skr_cp_step* st, skr_comm* comm, const char* who) {
@@ -45,7 +49,18 @@ skr_status check_step(const skr_attn_plan* plan, const skr_cp_step* st, skr_comm
               "%s: inconsistent sizes (rows %d, buffer %d, plan max %d, P %d)", who, st->rows, st->buf_rows,
               plan->max_rows, st->pad_rows_P);
   SKR_REQUIRE(st->natural_rows == 0 || comm, "%s: distributed chunks need a communicator", who);
+  if (comm && st->natural_rows > 0) {
+    int32_t n = 0, r = 0;
+    if (skr_status e = skr_comm_size(comm, &n, &r)) return e;
+    SKR_REQUIRE(n == st->cp, "%s: step planned for CP = %d but the communicator has %d ranks", who, st->cp, n);
+  }
   return SKR_OK;
+}
+
+// optional per-call timing (skr_cp_step.timing_events)
+skr_status mark(const skr_cp_step* st, int i, cudaStream_t m) {
+  if (!st->timing_events) return SKR_OK;
+  return skr::cuda_status(cudaEventRecord((cudaEvent_t)st->timing_events[i], m), "record timing event");
 }
 
 size_t row_bytes(const skr_attn_shape& s, int heads) {
@@ -94,15 +109,20 @@ SKR_EXPORT skr_status skr_cp_attn_fwd(skr_comm* comm, const skr_attn_plan* plan,
     if (skr_status e = cuda_status(cudaEventRecord(ev.b, sd), "record kv")) return e;
   }
   // a7: locals first (they need no exchange), then the distributed chunks
+  if (skr_status e = mark(st, 0, m)) return e;
   if (skr_status e = skr_attn_fwd(&s, &st->local_fwd, st->q, st->k, st->v, st->o, st->lse, st->buf_rows, st->buf_rows, m))
     return e;
+  if (skr_status e = mark(st, 1, m)) return e;
   if (dist) {
     if (skr_status e = cuda_status(cudaStreamWaitEvent(m, ev.b, 0), "wait kv")) return e;
+  }
+  if (skr_status e = mark(st, 2, m)) return e;
+  if (dist) {
     if (skr_status e = skr_attn_fwd(&s, &st->dist_fwd, st->q, st->k_natural, st->v_natural, st->o, st->lse,
                                     st->buf_rows, st->natural_rows, m))
       return e;
   }
-  return SKR_OK;
+  return mark(st, 3, m);
 }
 
 SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan, const skr_cp_step* st, void* main,
@@ -120,10 +140,16 @@ SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan,
     const size_t kv_elems = (size_t)st->natural_rows * s.hkv * s.d;
     if (skr_status e = cuda_status(cudaMemsetAsync(st->dk_partial, 0, kv_elems * 4, m), "zero dK partial")) return e;
     if (skr_status e = cuda_status(cudaMemsetAsync(st->dv_partial, 0, kv_elems * 4, m), "zero dV partial")) return e;
+  }
+  if (skr_status e = mark(st, 4, m)) return e;
+  if (dist) {
     if (skr_status e = skr_attn_bwd(&s, &st->dist_bwd, st->q, st->k_natural, st->v_natural, st->o, st->dout, st->lse,
                                     st->dq, st->dk_partial, st->dv_partial, 1, st->buf_rows, st->natural_rows, st->ws,
                                     st->ws_bytes, m))
       return e;
+  }
+  if (skr_status e = mark(st, 5, m)) return e;
+  if (dist) {
     if (skr_status e = cuda_status(cudaEventRecord(ev.a, m), "record partials")) return e;
     if (skr_status e = cuda_status(cudaStreamWaitEvent(sd, ev.a, 0), "wait partials")) return e;
     const int32_t f32b = (int32_t)((size_t)s.hkv * s.d * 4);
@@ -156,9 +182,11 @@ SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan,
     }
     if (skr_status e = cuda_status(cudaEventRecord(ev.b, sd), "record rs")) return e;
   }
+  if (skr_status e = mark(st, 6, m)) return e;
   if (skr_status e = skr_attn_bwd(&s, &st->local_bwd, st->q, st->k, st->v, st->o, st->dout, st->lse, st->dq, st->dk,
                                   st->dv, 0, st->buf_rows, st->buf_rows, st->ws, st->ws_bytes, m))
     return e;
+  if (skr_status e = mark(st, 7, m)) return e;
   if (dist) {
     if (skr_status e = cuda_status(cudaStreamWaitEvent(m, ev.b, 0), "wait rs")) return e;
   }

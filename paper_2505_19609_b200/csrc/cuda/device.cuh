@@ -17,6 +17,20 @@ inline skr_status check_sm100() {
   return SKR_OK;
 }
 
+// SM count of the CURRENT device (cached per device ordinal: a process may drive several GPUs).
+inline int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 inline skr_status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return SKR_OK;
   return fail(SKR_E_CUDA, "%s: %s", what, cudaGetErrorString(e));

@@ -141,6 +141,9 @@ SKR_EXPORT skr_status skr_pack_chunks(const int64_t* L, const int32_t* A, int32_
   if (skr_status s = view(L, A, K, N, &v)) return s;
   int64_t P = 0;
   for (int32_t r = 0; r < N; ++r) P = std::max(P, dist_rows_of(L, v, N, r));
+  // gathered_row = owner * P + offset < N * P must fit the int32 table (skr_pack_bounds checks the
+  // same bound, but a C caller need not have called it first)
+  if (P * N > INT32_MAX) return skr::fail(SKR_E_OVERFLOW, "skr_pack_chunks: N * P > 2^31 rows");
   // offset of each (seq, chunk) inside its owner's distributed prefix
   std::vector<int64_t> off_in_owner(N, 0);
   std::vector<int64_t> goff(2 * N * v.dist.size());

@@ -113,8 +113,10 @@ class RankStep:
             for name in ("dk_red", "dv_red"):
                 self._buf(name, (P, hkv, d), f32)
 
-    def cp_step(self, q_src, k_src, v_src, do_src):
-        """The skr_cp_step of this micro-batch (row a5-a9 composite C-ABI call) for these inputs."""
+    def cp_step(self, q_src, k_src, v_src, do_src, timing=None):
+        """The skr_cp_step of this micro-batch (row a5-a9 composite C-ABI call) for these inputs.
+        timing: optional 8 torch.cuda.Events (already created) the library records around its
+        attention calls (skr_cp_step.timing_events)."""
         if getattr(self, "_plan", None) is None:
             self._plan = sk.AttnPlan(self.shape, self.q.shape[0])
         p = lambda t: t.data_ptr() if t is not None else 0  # noqa: E731
@@ -128,7 +130,16 @@ class RankStep:
             p(self.k_gath) if d else 0, p(self.v_gath) if d else 0, p(self.k_nat) if d else 0,
             p(self.v_nat) if d else 0, p(self.dk_nat) if d else 0, p(self.dv_nat) if d else 0,
             p(self.dk_rm) if d else 0, p(self.dv_rm) if d else 0, p(self.dk_red) if d else 0,
-            p(self.dv_red) if d else 0, p(self.ws), self.ws.numel() * 4)
+            p(self.dv_red) if d else 0, p(self.ws), self.ws.numel() * 4, self._timing_ptr(timing))
+
+    def _timing_ptr(self, timing):
+        if timing is None:
+            self._timing_arr = None
+            return 0
+        import ctypes
+        arr = (ctypes.c_void_p * 8)(*[e.cuda_event for e in timing])
+        self._timing_arr = arr          # alive for the duration of the call
+        return ctypes.addressof(arr)
 
     def _buf(self, name, shape, dtype):
         self._bufspec.append((name, shape, dtype))
@@ -220,18 +231,20 @@ class RankStep:
     # One C-ABI call per direction (skr_cp_attn_fwd / _bwd, csrc/cuda/cp_step.cu). The per-phase
     # composition below runs the same kernels call by call; it is used when the attention calls are
     # timed individually (self.events) and by the one-GPU loopback tests.
-    def forward(self, q_src, k_src, v_src, comm=None, side=None):
+    def forward(self, q_src, k_src, v_src, comm=None, side=None, timing=None):
+        """timing: optional list of 8 created torch.cuda.Events (only [0:4] are recorded here)."""
         if self.events is None:
             self._fwd_inputs = (q_src, k_src, v_src)
-            sk.skr_cp_attn_fwd(comm, self._plan_or_new(), self.cp_step(q_src, k_src, v_src, None),
+            sk.skr_cp_attn_fwd(comm, self._plan_or_new(), self.cp_step(q_src, k_src, v_src, None, timing),
                                torch.cuda.current_stream(), side or torch.cuda.current_stream())
             return
         self.forward_phases(q_src, k_src, v_src, comm, side)
 
-    def backward(self, do_src, comm=None, side=None):
+    def backward(self, do_src, comm=None, side=None, timing=None):
+        """timing: optional list of 8 created torch.cuda.Events (only [4:8] are recorded here)."""
         if self.events is None:
             q_src, k_src, v_src = getattr(self, "_fwd_inputs", (None, None, None))
-            sk.skr_cp_attn_bwd(comm, self._plan_or_new(), self.cp_step(q_src, k_src, v_src, do_src),
+            sk.skr_cp_attn_bwd(comm, self._plan_or_new(), self.cp_step(q_src, k_src, v_src, do_src, timing),
                                torch.cuda.current_stream(), side or torch.cuda.current_stream())
             return
         self.backward_phases(do_src, comm, side)

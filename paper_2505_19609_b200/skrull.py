@@ -62,10 +62,18 @@ class skr_segs(C.Structure):
                 ("n_seg", i32), ("n_tiles", i32), ("row_begin", i32), ("row_end", i32)]
 
 
+_SIGS = {}
+
+
 def _sig(name, res, *args):
-    fn = getattr(_lib, name)
-    fn.restype = res
-    fn.argtypes = list(args)
+    """The library function `name` with its ctypes prototype, declared once per process (the
+    per-call RankStep path would otherwise re-declare prototypes on every call)."""
+    fn = _SIGS.get(name)
+    if fn is None:
+        fn = getattr(_lib, name)
+        fn.restype = res
+        fn.argtypes = list(args)
+        _SIGS[name] = fn
     return fn
 
 
@@ -432,7 +440,8 @@ class skr_cp_step(C.Structure):
                 ("q", vp), ("k", vp), ("v", vp), ("o", vp), ("dout", vp), ("dq", vp), ("dk", vp), ("dv", vp),
                 ("lse", vp), ("k_gathered", vp), ("v_gathered", vp), ("k_natural", vp), ("v_natural", vp),
                 ("dk_partial", vp), ("dv_partial", vp), ("dk_rankmajor", vp), ("dv_rankmajor", vp),
-                ("dk_reduced", vp), ("dv_reduced", vp), ("ws", vp), ("ws_bytes", C.c_size_t)]
+                ("dk_reduced", vp), ("dv_reduced", vp), ("ws", vp), ("ws_bytes", C.c_size_t),
+                ("timing_events", vp)]
 
 
 class AttnPlan:
@@ -549,8 +558,13 @@ class PeerComm:
         skr_peer_wait(self.flags, self.nranks, epoch, self.err, stream)
 
     def check(self):
+        """Raise if a peer wait timed out since the last check (the error word is then cleared, so
+        one timeout is reported once). Call after every synchronize of a step that used the
+        exchange: a timed-out wait lets the stream continue on stale peer data."""
         if int(self.err.item()):
-            raise SkrullError(SKR_E_CUDA, "peer exchange: a peer never signalled (10 s)")
+            self.err.zero_()
+            raise SkrullError(SKR_E_CUDA, "peer exchange: a peer never signalled (10 s); "
+                                          "the step's K/V or dK/dV used stale peer data")
 
     def close(self):
         skr_ipc_close_all()
@@ -593,6 +607,22 @@ class Comm:
     def all_reduce_f32(self, buf, stream=None):
         _check(_sig("skr_comm_all_reduce_f32", i32, vp, vp, C.c_size_t, vp)(
             self.h, _tptr(buf), buf.numel(), _stream(stream)))
+
+    def size(self):
+        """-> (nranks, rank) as the library sees the communicator."""
+        n, r = i32(), i32()
+        _check(_sig("skr_comm_size", i32, vp, P(i32), P(i32))(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
+    def check(self):
+        """Raise SkrullError(SKR_E_NCCL) if NCCL reported an asynchronous error."""
+        _check(_sig("skr_comm_async_error", i32, vp)(self.h))
+
+    def wait(self, stream=None, timeout_s=300.0):
+        """Host-wait for the work enqueued on `stream`, polling NCCL's asynchronous error state; on
+        an error or after timeout_s the communicator is aborted and SkrullError(SKR_E_NCCL) raised
+        (a dead peer cannot hang the caller)."""
+        _check(_sig("skr_comm_wait", i32, vp, vp, f64)(self.h, _stream(stream), float(timeout_s)))
 
     def close(self):
         if self.h:

@@ -1,9 +1,14 @@
 """Test harness: build packed varlen inputs from per-sequence synthetic tensors, run the CUDA path
 through the C-ABI binding, and compare with the fp64 oracle sequence by sequence.
 
-Tolerances (BASELINE.json north_star; readings R34 / R34'):
-  bf16: |gpu - oracle| <= 2e-2 + 2^-8 |oracle| elementwise, per tensor (O, dQ, dK, dV)
+Tolerances (BASELINE.json north_star; readings R34 / R34', DESIGN.md §9):
+  bf16: |gpu - oracle| <= 2e-2 + halfulp_bf16(max(|oracle|, |gpu|)) elementwise, per tensor
+        (O, dQ, dK, dV): the north_star's 2e-2 plus the exact representation error of storing the
+        result in bf16 (half the bf16 spacing at the value's binade; 0 below 2^-133)
   fp32: max |gpu - oracle| <= 1e-5 * max(1, max |oracle|)
+Every comparison is also recorded (plain max-abs error, count of elements above 2e-2, element
+count) and printed in the pytest terminal summary (tests/conftest.py), so the 2e-2 bar's plain
+max-abs figure is visible next to the R34' verdict.
 """
 from __future__ import annotations
 
@@ -13,25 +18,42 @@ from oracle.attention import attn_bwd, attn_fwd
 from synth import seq_tensors
 
 BF16_TOL = 2e-2
-BF16_REL = 2.0 ** -8
 FP32_TOL = 1e-5
 
+# (label, kind, max_abs, n_above_2e-2, n) of every comparison in this process
+STATS = []
 
-def tol_ok(got, ref, fp32: bool):
-    """bf16 (R34'): |gpu - ref| <= 2e-2 + 2^-8 |ref| elementwise -- the north_star's 2e-2 absolute
-    bar plus the bf16 representation term (a bf16 value of magnitude >= 8 cannot be stored within
-    2e-2 of the exact result; P / dS enter the tensor-core GEMMs as bf16, R31).
+
+def halfulp_bf16(x):
+    """Half the spacing of the bf16 grid at |x| (8 significant bits): 2^(floor(log2|x|) - 8),
+    i.e. the largest error of rounding a real of that binade to bf16; 0 for x == 0."""
+    a = np.abs(np.asarray(x, np.float64))
+    _, e = np.frexp(a)                      # a = m 2^e, m in [0.5, 1): floor(log2 a) = e - 1
+    return np.where(a > 0, np.ldexp(1.0, e - 9), 0.0)
+
+
+def tol_ok(got, ref, fp32: bool, label: str = ""):
+    """bf16 (R34'): |gpu - ref| <= 2e-2 + halfulp_bf16(max(|ref|, |gpu|)) elementwise -- the
+    north_star's 2e-2 absolute bar plus the exact error of representing the result in the bf16 it
+    is stored in (above |x| = 4 the bf16 grid itself is coarser than 2e-2; P / dS also enter the
+    tensor-core GEMMs as bf16, R31). The larger magnitude is used because a result within 2e-2 of
+    a power of two may round into the next binade.
     fp32 (R34): max |gpu - ref| <= 1e-5 * max(1, max |ref|).
-    Returns (ok, worst abs error, bound at the worst element)."""
+    Returns (ok, worst abs error, bound at the worst element); records the plain max-abs error and
+    the count of elements above 2e-2 in STATS."""
     if ref.size == 0:
         return True, 0.0, 0.0
-    diff = np.abs(got.astype(np.float64) - ref)
+    got64 = got.astype(np.float64)
+    diff = np.abs(got64 - ref)
+    nan = bool(np.isnan(got64).any())
+    STATS.append((label, "fp32" if fp32 else "bf16", float(np.nanmax(diff)) if not nan else float("nan"),
+                  int((diff > BF16_TOL).sum()), int(diff.size)))
     if fp32:
         bound = FP32_TOL * max(1.0, float(np.max(np.abs(ref))))
-        return bool(np.all(diff <= bound)) and not np.isnan(got).any(), float(diff.max()), bound
-    bnd = BF16_TOL + BF16_REL * np.abs(ref)
+        return bool(np.all(diff <= bound)) and not nan, float(diff.max()), bound
+    bnd = BF16_TOL + halfulp_bf16(np.maximum(np.abs(ref), np.abs(got64)))
     i = int(np.argmax(diff - bnd))
-    ok = bool(np.all(diff <= bnd)) and not np.isnan(got).any()
+    ok = bool(np.all(diff <= bnd)) and not nan
     return ok, float(diff.flat[i]), float(bnd.flat[i])
 
 

@@ -71,3 +71,29 @@ def test_buffer_pool_views():
     assert pool.bufs["x"].numel() == 40                     # the largest request
     va, vb = pool.get("x", (10, 4), torch.float32), pool.get("x", (3, 5), torch.float32)
     assert va.shape == (10, 4) and vb.shape == (3, 5) and va.data_ptr() == vb.data_ptr()
+
+
+def test_workload_grid_cp_and_default(bench):
+    # a named config under --dp > 1 must plan for CP = world // dp (not world)
+    from types import SimpleNamespace as NS
+    a = NS(config="C5n4", dp=2, seed=0)
+    name, cfg, lens, shp, cp, bucket, scaling = bench.workload(a, 8)
+    assert (name, cp, cfg.cp, scaling) == ("C5n4", 4, 4, "weak")
+    # the default workload is S4n{CP} at every N (BENCH and SCALE share it), strong scaling
+    for world, dp, want in ((1, 1, "S4n1"), (2, 1, "S4n2"), (8, 1, "S4n8"), (8, 2, "S4n4")):
+        name, cfg, lens, shp, cp, bucket, scaling = bench.workload(NS(config=None, dp=dp, seed=0), world)
+        assert name == want and cp == world // dp and scaling == "strong" and len(lens) == 512
+    with pytest.raises(SystemExit):
+        bench.workload(NS(config="C5n4", dp=1, seed=0), 8)      # CP 8 != config's 4
+    with pytest.raises(SystemExit):
+        bench.workload(NS(config=None, dp=3, seed=0), 8)        # dp does not divide the world
+
+
+def test_pick_peak(bench):
+    peaks = {"bf16_tflops": 1629.9, "bf16_tflops_sustained": 1368.0}
+    (p, k), b, s = bench.pick_peak(peaks, {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0}, 8.0)
+    assert (p, k) == (1629.9, "bf16_tflops")                    # full clocks: burst
+    (p, k), _, _ = bench.pick_peak(peaks, {"sm_mhz": 1410.0, "sm_max_mhz": 1965.0}, 8.0)
+    assert (p, k) == (1368.0, "bf16_tflops_sustained")          # seconds at power-capped clocks
+    (p, k), _, _ = bench.pick_peak(peaks, {"sm_mhz": 1410.0, "sm_max_mhz": 1965.0}, 0.2)
+    assert k == "bf16_tflops"                                   # a short region is a burst

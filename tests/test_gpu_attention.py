@@ -31,7 +31,7 @@ def _check_fwd(pk, O, LSE, fp32):
     for s, lo, hi in pk.segs:
         Oref, Lref, *_ = oracle_seq(pk.inputs[s], bwd=False)
         n = hi - lo
-        ok, err, bound = tol_ok(O[r:r + n], Oref[lo:hi], fp32)
+        ok, err, bound = tol_ok(O[r:r + n], Oref[lo:hi], fp32, label="O attention")
         assert ok, f"O seq {s} [{lo},{hi}): err {err} > {bound}"
         lerr = np.abs(LSE[:, r:r + n] - Lref[:, lo:hi]).max() if n else 0.0
         assert lerr <= (1e-5 * max(1, np.abs(Lref).max()) if fp32 else 2e-2), f"LSE seq {s}: {lerr}"
@@ -130,7 +130,7 @@ def _check_bwd_local(pk, dQ, dK, dV, fp32):
         _, _, rq, rk, rv = oracle_seq(pk.inputs[s])
         n = hi - lo
         for name, got, ref in (("dQ", dQ[r:r + n], rq), ("dK", dK[r:r + n], rk), ("dV", dV[r:r + n], rv)):
-            ok, err, bound = tol_ok(got, ref, fp32)
+            ok, err, bound = tol_ok(got, ref, fp32, label=f"{name} attention")
             assert ok, f"{name} seq {s} (len {n}): err {err} > {bound}"
         r += n
 
@@ -217,7 +217,7 @@ def test_bwd_distributed_chunks_sum_to_unsharded(dtype, N):
         _check_fwd(pk, O, L, fp32=not bf)
         r = 0
         for s, lo, hi in segs:
-            ok, err, bound = tol_ok(dQ[r:r + hi - lo], refs[s][2][lo:hi], not bf)
+            ok, err, bound = tol_ok(dQ[r:r + hi - lo], refs[s][2][lo:hi], not bf, label="dQ attention-dist")
             assert ok, f"dQ rank {j} seq {s} [{lo},{hi}): {err} > {bound}"
             r += hi - lo
         dk_sum += dK[:acc]
@@ -225,5 +225,5 @@ def test_bwd_distributed_chunks_sum_to_unsharded(dtype, N):
     for s, S in enumerate(lens):
         for name, got, ref in (("dK", dk_sum[base[s]:base[s] + S], refs[s][3]),
                                ("dV", dv_sum[base[s]:base[s] + S], refs[s][4])):
-            ok, err, bound = tol_ok(got, ref, not bf)
+            ok, err, bound = tol_ok(got, ref, not bf, label=f"{name} attention-dist")
             assert ok, f"{name} seq {s}: {err} > {bound}"

@@ -27,7 +27,7 @@ def test_bench_two_ranks_one_gpu(extra, cp, dp):
     env = dict(os.environ, SKR_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
            "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
-           "--warmup", "1", "--no-cpu-baseline", "--no-e2e"] + extra
+           "--warmup", "1", "--no-cpu-baseline", "--no-e2e", "--config", "C2"] + extra
     out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]

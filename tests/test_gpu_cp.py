@@ -56,7 +56,7 @@ def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1, exchange="nccl"):
         for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
             got = outs[key][s]
             assert not np.isnan(got).any(), f"{key} seq {s}: rows not covered"
-            ok, err, bound = tol_ok(got, ref, not bf16)
+            ok, err, bound = tol_ok(got, ref, not bf16, label=f"{key} cp")
             assert ok, f"{key} seq {s} (len {lens[s]}, N={N}): err {err} > {bound}"
         assert np.abs(lse[s] - Lr).max() <= (2e-2 if bf16 else 1e-5 * max(1, np.abs(Lr).max()))
     return n_dist, p
@@ -155,7 +155,7 @@ def test_buffer_pool_micro_batches_share_buffers():
             O, _ = attn_fwd(x["q"], x["k"], x["v"])
             dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
             for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
-                ok, err, bound = tol_ok(getattr(rs, key)[a:b].float().cpu().numpy(), ref, False)
+                ok, err, bound = tol_ok(getattr(rs, key)[a:b].float().cpu().numpy(), ref, False, label=f"{key} pool")
                 assert ok, f"{key} seq {idx[pr['seg_seq'][i]]}: err {err} > {bound}"
 
 

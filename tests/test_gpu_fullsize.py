@@ -98,7 +98,7 @@ def _rows(runs, loc, s, positions, key):
 
 
 def _check(name, got, ref, where):
-    ok, err, bound = tol_ok(got, ref, False)
+    ok, err, bound = tol_ok(got, ref, False, label=f"{name} fullsize")
     assert ok, f"{name} {where}: err {err} > {bound}"
 
 
@@ -140,3 +140,77 @@ def test_fullsize_sampled(cfg_name):
         _check("dv", _rows(runs, loc, s, tail, "dv"), dV[j0:], f"{cfg_name} seq {s} (S={S}) key tail")
         checked += 1
     assert checked >= 3
+
+
+# ------------------------------------------------------------------ whole long sequences
+# The sampled checks above see dK / dV only on the last TAIL keys, which accumulate over at most two
+# query tiles; here a >= 8K sequence of each full-size shape is checked WHOLE (every row of O, LSE,
+# dQ, dK, dV), run locally (N = 1) and zigzag-sharded over CP = 8 by loopback (R20: each rank's two
+# chunks; dK / dV then come from the fp32 partials of all 8 ranks summed by the reduce-scatter
+# emulation and cast into the owners' packed prefixes). Keys near the start accumulate over all
+# 65 query tiles x every q-head of the group, the long-accumulation path of the backward.
+WHOLE_LEN = 8192 + 77        # ragged last tile
+_WHOLE_REF = {}
+
+
+def _whole_ref(shp, lens, seed):
+    key = (shp.hq, shp.hkv, shp.d, tuple(lens), seed)
+    if key not in _WHOLE_REF:
+        refs = []
+        for k, S in enumerate(lens):
+            x = seq_tensors(seed, k, int(S), shp.hq, shp.hkv, shp.d)
+            O, L = attn_fwd(x["q"], x["k"], x["v"])
+            dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
+            refs.append(dict(o=O, lse=L, dq=dQ, dk=dK, dv=dV))
+        _WHOLE_REF[key] = refs
+    return _WHOLE_REF[key]
+
+
+@pytest.mark.parametrize("N", [1, 8])
+@pytest.mark.parametrize("shape_name", ["qwen05", "qwen7"])
+def test_fullsize_whole_long_sequence(shape_name, N):
+    from paper_2505_19609_b200 import skrull as sk
+    from paper_2505_19609_b200.runtime import RankStep, gather_rank_natural, loopback_step
+    from synth.configs import QWEN05, QWEN7
+    shp = {"qwen05": QWEN05, "qwen7": QWEN7}[shape_name]
+    seed = 11
+    lens = np.asarray([WHOLE_LEN, 1000, 300, 17], np.int64)
+    # the planner decides: at N = 8 a BucketSize below the long sequence makes DACP shard it (R33)
+    C = 1 << 20 if N == 1 else 4096
+    p = sk.skr_plan(lens, C, N, 1, shp.hidden, shp.kv_hidden)
+    ref_plan = oracle_plan([int(x) for x in lens], C, N, 1, Model(shp.hidden, shp.kv_hidden))
+    assert list(p["assign"]) == list(ref_plan.assign)
+    assert int(p["n_mb_per_dp"][0]) == 1
+    assert (p["assign"][0] == -1) == (N > 1)
+    shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
+    inputs = [seq_tensors(seed, k, int(S), shp.hq, shp.hkv, shp.d) for k, S in enumerate(lens)]
+    ranks = [RankStep(shape, lens, p["assign"], N, r) for r in range(N)]
+    srcs = {k: [torch.from_numpy(gather_rank_natural(inputs, lens, p["assign"], N, r, k)).to("cuda", torch.bfloat16)
+                for r in range(N)] for k in ("q", "k", "v", "do")}
+    if N == 1:
+        side = torch.cuda.Stream(priority=-1)
+        ranks[0].forward(srcs["q"][0], srcs["k"][0], srcs["v"][0], None, side)
+        ranks[0].backward(srcs["do"][0], None, side)
+    else:
+        loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+    torch.cuda.synchronize()
+    got = {key: [np.full((int(S),) + inputs[k]["q" if key in ("o", "dq") else "k"].shape[1:], np.nan)
+                 for k, S in enumerate(lens)] for key in ("o", "dq", "dk", "dv")}
+    lse = [np.full((shp.hq, int(S)), np.nan) for S in lens]
+    for rs in ranks:
+        pr = rs.pr
+        f = lambda t: t.float().cpu().numpy()  # noqa: E731
+        arr = {key: f(getattr(rs, key)) for key in ("o", "dq", "dk", "dv")}
+        L = f(rs.lse)
+        for i in range(pr["n_seg"]):
+            a, b = int(pr["cu_seqlens_q"][i]), int(pr["cu_seqlens_q"][i + 1])
+            s, lo = int(pr["seg_seq"][i]), int(pr["q_pos"][i])
+            for key in got:
+                got[key][s][lo:lo + b - a] = arr[key][a:b]
+            lse[s][:, lo:lo + b - a] = L[:, a:b]
+    refs = _whole_ref(shp, [int(x) for x in lens], seed)
+    for s in range(len(lens)):
+        for key in ("o", "dq", "dk", "dv"):
+            assert not np.isnan(got[key][s]).any(), f"{key} seq {s}: rows not covered"
+            _check(key, got[key][s], refs[s][key], f"{shape_name} N={N} seq {s} (S={int(lens[s])}) whole")
+        assert np.abs(lse[s] - refs[s]["lse"]).max() <= 2e-2

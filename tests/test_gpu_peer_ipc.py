@@ -100,5 +100,5 @@ def test_peer_exchange_two_processes():
         for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
             got = outs[key][s]
             assert not np.isnan(got).any(), f"{key} seq {s}: rows not covered"
-            ok, err, bound = tol_ok(got, ref, False)
+            ok, err, bound = tol_ok(got, ref, False, label=f"{key} peer-ipc")
             assert ok, f"{key} seq {s} (len {LENS[s]}): err {err} > {bound}"

@@ -150,14 +150,11 @@ def test_heuristic_never_beats_optimum_and_gap_guard():
         assert h >= opt[1]
         ratios.append(h / opt[1])
         n_done += 1
-    # The <= 2.0 guard of S:561 is an empirical regression guard, not a theorem: on this
-    # instance family the worst case is 3.10 (a forced shard pays T_fixed that the optimum
-    # avoids). Guard the distribution instead (values measured when the test was frozen).
-    ratios.sort()
-    # (median 1.19, p95 2.32, max 3.10 at freeze time)
-    assert ratios[len(ratios) // 2] <= 1.25
-    assert ratios[int(0.95 * len(ratios))] <= 2.4
-    assert ratios[-1] <= 3.2
+    # S:561's "max ratio <= 2.0" is an empirical statement about ITS instance family, not a
+    # theorem (reading R37): on this family a forced shard can pay the fixed T_comm the optimum
+    # avoids, so only the proven property -- the heuristic never beats the optimum -- is asserted
+    # (above). No distribution of this oracle's own ratios is frozen as a pin.
+    assert len(ratios) == 200
 
 
 def test_lpt():
@@ -212,6 +209,30 @@ def test_gds_interleave_separates_longest():
     top = sorted(range(8), key=lambda k: -lens[k])[:init]
     for mb in mbs:
         assert len(set(mb) & set(top)) <= 1
+
+
+def test_joint_optimum_hand_computed():
+    # optimal_joint_ws1 pinned to exact values worked by hand from Eq. 1-5 and Eq. 8-10
+    # with the S:241 toy model (h = h_kv = b = 1: FLOPs(S) = 24 S + 4 S^2,
+    # Volume(S) = S) and identity fits (T_comp = FLOPs, T_comm = Volume, T_comm(0) = 0, R26):
+    #   FLOPs(1) = 28, FLOPs(2) = 64, FLOPs(4) = 160, FLOPs(6) = 288.
+    # [2,2], N=2, C=2: one micro-batch with the two sequences local on ranks 0 / 1 -> max(0, 64) = 64;
+    #   both distributed: 4 + 128/2 = 68; split {2},{2}: each best distributed 2 + 32 = 34 -> 68. => 64
+    assert optimal_joint_ws1([2, 2], 2, 2, TOY, ID, ID) == 64
+    # [4,4], N=2, C=4: locals on separate ranks 160; both distributed 8 + 160 = 168 (mixed: rank
+    #   memory 4 + 2 > C); split: 2 x (4 + 80) = 168. => 160
+    assert optimal_joint_ws1([4, 4], 4, 2, TOY, ID, ID) == 160
+    # [1,1,6], N=2, C=4 (Eq. 10: C*N = 8 = sum): 6 must be distributed (6 > C). One micro-batch:
+    #   1s local on ranks 0 / 1 (memory 3 + 1 = 4): max(6, 28) + 288/2 = 172; all distributed
+    #   8 + 344/2 = 180. Splits: {6},{1,1}: 150 + 28 = 178; {6,1},{1}: 165 + 15 = 180;
+    #   {6},{1},{1}: 150 + 15 + 15 = 180. => 172 (a max over micro-batches instead of Eq. 8's sum
+    #   would give 150)
+    assert optimal_joint_ws1([1, 1, 6], 4, 2, TOY, ID, ID) == 172
+    # [4,4,4], N=2, C=4: sum 12 > C*N, so at least two micro-batches (Eq. 10): {4,4},{4}:
+    #   160 + 84 = 244; {4},{4},{4}: 3 x 84 = 252. => 244
+    assert optimal_joint_ws1([4, 4, 4], 4, 2, TOY, ID, ID) == 244
+    # a single sequence longer than C*N has no feasible partition
+    assert optimal_joint_ws1([9], 4, 2, TOY, ID, ID) is None
 
 
 def test_joint_bruteforce_bounds_heuristic():
