@@ -438,7 +438,7 @@ def run_ours(args):
         kt = {"fwd": 0.0, "bwd": 0.0}
         for rs, _ in steps:
             for kind, a, b in rs.events:
-                kt[kind] += a.elapsed_time(b)
+                kt[kind[:3]] += a.elapsed_time(b)
             rs.events = None
         fwd_ms, bwd_ms = kt["fwd"] / K, kt["bwd"] / K
 

@@ -52,11 +52,10 @@ __device__ __forceinline__ void trace(int ev) {
 }
 
 constexpr int BN = 128;  // key tile
-// Grid order: 0 = (KV head, key tile) with the head fastest; 1 = (key tile, KV head), every key
-// tile of one KV head before the next, so the CTAs in flight share one group's Q / dO / dQ rows.
-#ifndef SKR_GRID_HEAD_MAJOR
-#define SKR_GRID_HEAD_MAJOR 0
-#endif
+// Grid order (launch argument head_major): 0 = (KV head, key tile) with the head fastest; 1 = (key
+// tile, KV head), every key tile of one KV head before the next, so the CTAs in flight share one
+// group's Q / dO / dQ rows. d = 128 uses 1 (S4n1 bwd DRAM 166 -> 120 GB per launch, C5n1 bwd
+// -5 %); d = 64 keeps 0 (profiles/r02_experiments.md).
 constexpr int kThreads = 448;
 constexpr int kComputeThreads = 256;
 
@@ -141,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, AttnArgs a, const float* __restrict__ lse,
                     const float* __restrict__ Dbuf, void* __restrict__ dk_out, void* __restrict__ dv_out,
-                    int accumulate, float* __restrict__ dq_acc) {
+                    int accumulate, float* __restrict__ dq_acc, int head_major) {
   using C = Cfg<D>;
   constexpr int BQ = C::BQ, H = C::H;
   extern __shared__ uint8_t smem_raw[];
@@ -150,8 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* aux = reinterpret_cast<float*>(smem + C::kOffAux);  // lse2[kStages][BQ] then dd[kStages][BQ]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
-  const int g = SKR_GRID_HEAD_MAJOR ? blockIdx.y : blockIdx.x;
-  const int bt = SKR_GRID_HEAD_MAJOR ? blockIdx.x : blockIdx.y;
+  const int g = head_major ? blockIdx.y : blockIdx.x;
+  const int bt = head_major ? blockIdx.x : blockIdx.y;
   const int seg = a.tiles[2 * bt], ktile = a.tiles[2 * bt + 1];
   const int grp = a.hq / a.hkv;
   const int cu0 = a.cu[seg], q_len = a.cu[seg + 1] - cu0;
@@ -834,7 +833,8 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
         !make_tmap_2d(&tdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n_q_rows, qcols, qcols,
                       d == 128 ? 32 : bq, 32, true))   // d = 128 reduces in 32-query halves
       return fail(SKR_E_CUDA, "attn bwd: tensor map encode failed");
-    dim3 grid = SKR_GRID_HEAD_MAJOR ? dim3(a.n_tiles, a.hkv) : dim3(a.hkv, a.n_tiles);
+    const int head_major = d == 128 ? 1 : 0;
+    dim3 grid = head_major ? dim3(a.n_tiles, a.hkv) : dim3(a.hkv, a.n_tiles);
     // share of exponentials on the FMA pipe; SKR_BWD_POLY (0-3) overrides for sweeps
     static int poly = [] {
       const char* e = getenv("SKR_BWD_POLY");
@@ -846,7 +846,8 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
     const int pp = poly >= 0 ? poly : (d == 64 ? 1 : 0);
     auto launch = [&](auto kern, int smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      kern<<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv, accumulate, dq_acc);
+      kern<<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv, accumulate, dq_acc,
+                                              head_major);
     };
     if (d == 128) {
       constexpr int smem = bwd::Cfg<128>::kSmem;

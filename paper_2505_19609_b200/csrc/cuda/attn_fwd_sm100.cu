@@ -78,14 +78,11 @@ __device__ __forceinline__ void trace_smw(int, int) {}
 
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 576;
-// Grid order of the two-head kernel: 0 = (head pair, tile) with the pair fastest; 1 = (tile, head
-// pair), every tile of one pair before the next pair, so the CTAs in flight share one KV head's K / V
-// (L2-resident) instead of streaming every head's.
-#ifndef SKR_GRID_HEAD_MAJOR
-#define SKR_GRID_HEAD_MAJOR 0
-#endif
-__device__ __forceinline__ int blk_pair() { return SKR_GRID_HEAD_MAJOR ? blockIdx.y : blockIdx.x; }
-__device__ __forceinline__ int blk_tile() { return SKR_GRID_HEAD_MAJOR ? blockIdx.x : blockIdx.y; }
+// Grid order of the two-head kernel (launch argument head_major): 0 = (head pair, tile) with the
+// pair fastest; 1 = (tile, head pair), every tile of one pair before the next pair, so the CTAs in
+// flight share one KV head's K / V (L2-resident) instead of streaming every head's. d = 128 uses 1:
+// S4n1 fwd DRAM 52 -> 9.4 GB per launch, S4n1 / C5n1 +2 % / +6 % (profiles/r02_experiments.md);
+// d = 64 keeps 0 (a 32K sequence's K / V is 8 MB per head, L2-resident either way; 1 measured -1.5 %).
 constexpr int kSoftmax = 256;                // threads per head (two warpgroups)
 constexpr int kTmaWarp = 16, kMmaWarp = 17;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -130,8 +127,9 @@ template <int D, int kPolyPer8>   // kPolyPer8: exponentials per 8 computed by e
 __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers per thread
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
-                    float* __restrict__ lse, int pairs_per_group) {
+                    float* __restrict__ lse, int pairs_per_group, int head_major) {
   using C = Cfg<D>;
+  const int blk_pair = head_major ? blockIdx.y : blockIdx.x, blk_tile = head_major ? blockIdx.x : blockIdx.y;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -147,17 +145,17 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
   const int grp = a.hq / a.hkv;
   int ha, hb;
   if (pairs_per_group == 0) {
-    ha = 2 * blk_pair();
+    ha = 2 * blk_pair;
     hb = (ha + 1 < a.hq) ? ha + 1 : -1;
   } else {
-    const int g = blk_pair() / pairs_per_group, p = blk_pair() % pairs_per_group;
+    const int g = blk_pair / pairs_per_group, p = blk_pair % pairs_per_group;
     ha = g * grp + 2 * p;
     hb = (2 * p + 1 < grp) ? ha + 1 : -1;
   }
   const int ga = ha / grp, gb = hb >= 0 ? hb / grp : ga;
   const bool xg = D == 128 && gb != ga;                // compile-time false for d = 64 (per-group pairs)
   const int U = xg ? 4 : 2;                             // ring units per KV tile
-  const int seg = a.tiles[2 * blk_tile()], tile = a.tiles[2 * blk_tile() + 1];
+  const int seg = a.tiles[2 * blk_tile], tile = a.tiles[2 * blk_tile + 1];
   const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
   const int r0 = cu0 + tile * BM;                       // first packed query row of the tile
   const int n_valid = min(BM, cu1 - r0);
@@ -1068,7 +1066,8 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   // d = 64: pairs within each group
   const int ppg = d == 128 ? 0 : (a.hq / a.hkv + 1) / 2;
   const int n_pairs = d == 128 ? (a.hq + 1) / 2 : a.hkv * ppg;
-  dim3 grid = SKR_GRID_HEAD_MAJOR ? dim3(a.n_tiles, n_pairs) : dim3(n_pairs, a.n_tiles);
+  const int head_major = d == 128 ? 1 : 0;
+  dim3 grid = head_major ? dim3(a.n_tiles, n_pairs) : dim3(n_pairs, a.n_tiles);
   // share of exponentials on the FMA pipe (MUFU ex2 bounds the d = 64 forward); SKR_FWD_POLY overrides
   static int poly = [] {
     const char* e = getenv("SKR_FWD_POLY");
@@ -1080,7 +1079,7 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   const int pp = poly >= 0 ? poly : (d == 64 ? 2 : 1);
   auto launch = [&](auto kern, int smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg);
+    kern<<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg, head_major);
   };
   // d = 128, one head per CTA (double-buffered S, separate P): opt-in, SKR_FWD_1H=1 (measured slower:
   // without the GQA head pair each K/V tile is loaded and read per head, profiles/r01_experiments.md)

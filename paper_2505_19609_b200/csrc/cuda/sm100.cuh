@@ -366,16 +366,20 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return d;
 }
 
-// 2^x on the FMA/ALU pipes (no MUFU): x = i + f, f in [0,1); 2^f by a degree-3 minimax polynomial
-// (max relative error 8.8e-5, far below the bf16 rounding of P), 2^i by adding i to the exponent.
-// Inputs below -126 flush to ~2^-126 (a masked score contributes < 1.2e-38).
+// 2^x on the FMA/ALU pipes (no MUFU): x = i + f, f in [0,1); 2^f by a degree-3 polynomial with
+// p(0) = 1, minimax in relative error on [0, 1) (fitted by tools/fit_ex2_poly.py, an LP on a dense
+// grid; fp32 Horner evaluation max relative error 8.6e-5, pinned by tests/test_ex2_poly.py -- far
+// below the bf16 rounding of P), 2^i by adding i to the exponent. The range reduction rounds x
+// down by adding 1.5 * 2^23 in round-toward-minus-infinity (the technique FlashAttention-4's
+// exp2 emulation also uses). Inputs below -126 flush to ~2^-126 (a masked score contributes
+// < 1.2e-38).
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -126.f);
   const float t = __fadd_rd(x, 12582912.f);              // 1.5 * 2^23: floor(x) in the low mantissa bits
   const int i = __float_as_int(t) - 0x4B400000;
   const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 0.077119089663028717041015625f, 0.227564394474029541015625f);
-  p = fmaf(p, f, 0.695146143436431884765625f);
+  float p = fmaf(f, 0.077068030834198f, 0.22764353454113007f);
+  p = fmaf(p, f, 0.6951172947883606f);
   p = fmaf(p, f, 1.0f);
   return __int_as_float(__float_as_int(p) + (i << 23));
 }

@@ -82,7 +82,8 @@ class RankStep:
         nd, ns = pr["n_dist_seg"], pr["n_seg"]
         cu, qp, ks, kl = pr["cu_seqlens_q"], pr["q_pos"], pr["k_start"], pr["k_len"]
         self.has_dist = self.nat_rows > 0
-        self.events = None          # list -> (kind, start, end) CUDA events around attention calls
+        self.events = None          # list -> (kind, start, end) CUDA events around attention calls;
+        #                             kind in fwd_local / fwd_dist / bwd_dist / bwd_local
         self.src_row = torch.as_tensor(pr["src_row"]).to(device)
         # segment classes: distributed chunks [0, nd), locals [nd, ns)
         self.dist_f = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "fwd", device)
@@ -195,17 +196,17 @@ class RankStep:
         self.events.append((kind, e0, e1))
 
     def fwd_local(self, stream=None):
-        self._timed("fwd", lambda: sk.skr_attn_fwd(self.shape, self.loc_f, self.q, self.k, self.v, self.o, self.lse,
+        self._timed("fwd_local", lambda: sk.skr_attn_fwd(self.shape, self.loc_f, self.q, self.k, self.v, self.o, self.lse,
                                                    stream), stream)
 
     def fwd_dist(self, stream=None):
-        self._timed("fwd", lambda: sk.skr_attn_fwd(self.shape, self.dist_f, self.q, self.k_nat, self.v_nat, self.o,
+        self._timed("fwd_dist", lambda: sk.skr_attn_fwd(self.shape, self.dist_f, self.q, self.k_nat, self.v_nat, self.o,
                                                    self.lse, stream), stream)
 
     def bwd_dist(self, stream=None):
         self.dk_nat.zero_()
         self.dv_nat.zero_()
-        self._timed("bwd", lambda: sk.skr_attn_bwd(self.shape, self.dist_b, self.q, self.k_nat, self.v_nat, self.o,
+        self._timed("bwd_dist", lambda: sk.skr_attn_bwd(self.shape, self.dist_b, self.q, self.k_nat, self.v_nat, self.o,
                                                    self.do, self.lse, self.dq, self.dk_nat, self.dv_nat, 1, self.ws,
                                                    stream), stream)
 
@@ -224,7 +225,7 @@ class RankStep:
                 sk.skr_cast_f32_bf16(self.dv_red[:n], self.dv[:n], stream)
 
     def bwd_local(self, stream=None):
-        self._timed("bwd", lambda: sk.skr_attn_bwd(self.shape, self.loc_b, self.q, self.k, self.v, self.o, self.do,
+        self._timed("bwd_local", lambda: sk.skr_attn_bwd(self.shape, self.loc_b, self.q, self.k, self.v, self.o, self.do,
                                                    self.lse, self.dq, self.dk, self.dv, 0, self.ws, stream), stream)
 
     # ------------------------------------------------------------------ production composition

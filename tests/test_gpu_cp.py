@@ -14,15 +14,47 @@ from oracle.cost_model import Model  # noqa: E402
 from tests.attn_harness import make_inputs, tol_ok  # noqa: E402
 
 
-def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1, exchange="nccl"):
+def _baseline_plan(sk, lens, C, N, planner):
+    """Row f1: the paper's baselines as plans the same runtime executes (one DP rank). 'rr' /
+    'rr_norb': Alg. 4 round-robin with / without roll-back (P:492-515, R27) on one micro-batch;
+    'full_shard': FIFO micro-batches under C*N (Eq. 10), every sequence distributed (the
+    DeepSpeed-like CP of P:101). Bit-exact against the oracle's implementations."""
+    from oracle.schedule import ScheduleError, full_shard, round_robin
+    K = len(lens)
+    if planner in ("rr", "rr_norb"):
+        rb = planner == "rr"
+        try:
+            ref = round_robin(list(lens), C, N, rb)
+        except ScheduleError:
+            with pytest.raises(sk.SkrullError):
+                sk.skr_round_robin(lens, C, N, rb)
+            return None
+        A, _ = sk.skr_round_robin(lens, C, N, rb)
+        assert list(A) == ref                                     # bit-exact baseline plan
+        return dict(dp_of_seq=np.zeros(K, np.int32), mb_of_seq=np.zeros(K, np.int32), assign=np.asarray(A),
+                    n_mb_per_dp=np.asarray([1], np.int32), n_rollbacks=0)
+    mbs = full_shard(list(lens), C, N)
+    M, n = sk.skr_full_shard(lens, C, N)
+    assert n == len(mbs) and all(M[k] == j for j, mb in enumerate(mbs) for k in mb)
+    return dict(dp_of_seq=np.zeros(K, np.int32), mb_of_seq=np.asarray(M), assign=np.full(K, -1, np.int32),
+                n_mb_per_dp=np.asarray([n], np.int32), n_rollbacks=0)
+
+
+def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1, exchange="nccl", planner="skrull"):
     from paper_2505_19609_b200 import skrull as sk
     from paper_2505_19609_b200.runtime import (RankStep, dp_micro_batches, gather_rank_natural, loopback_peer_step,
                                                loopback_step)
     shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16 if bf16 else sk.SKR_FP32)
-    p = sk.skr_plan(lens, C, N, dp, hq * d, hkv * d)
-    ref = oracle_plan(list(lens), C, N, dp, Model(hq * d, hkv * d))
-    assert list(p["assign"]) == ref.assign                       # bit-exact plan
-    assert list(p["dp_of_seq"]) == ref.dp_of_seq and list(p["mb_of_seq"]) == ref.mb_of_seq
+    if planner == "skrull":
+        p = sk.skr_plan(lens, C, N, dp, hq * d, hkv * d)
+        ref = oracle_plan(list(lens), C, N, dp, Model(hq * d, hkv * d))
+        assert list(p["assign"]) == ref.assign                       # bit-exact plan
+        assert list(p["dp_of_seq"]) == ref.dp_of_seq and list(p["mb_of_seq"]) == ref.mb_of_seq
+    else:
+        assert dp == 1
+        p = _baseline_plan(sk, lens, C, N, planner)
+        if p is None:                                   # the baseline fails (Table 3 "OOM"), as the oracle does
+            return None, None
     inputs = make_inputs(lens, hq, hkv, d, seed=seed, bf16=bf16)
     tdt = torch.bfloat16 if bf16 else torch.float32
     src_key = {"o": "q", "dq": "q", "dk": "k", "dv": "k"}
@@ -177,3 +209,25 @@ def test_random_plans_fuzz(case):
     C = rng.randint(lo, max(lo, sum(lens) // N + 256))
     # every 6th case in fp32 test mode; every 3rd through the row-f3 peer-memory exchange
     _run(lens, hq, hkv, d, N, C, case % 6 != 5, 50 + case, exchange="peer" if case % 3 == 1 else "nccl")
+
+
+@pytest.mark.parametrize("planner", ["rr", "rr_norb", "full_shard"])
+@pytest.mark.parametrize("case", range(6))
+def test_baseline_plans_fuzz(planner, case):
+    # row f1: the baselines' plans (round-robin Alg. 4 with / without roll-back, full-shard CP)
+    # through the same CP runtime and kernels, every output against the fp64 oracle
+    import random
+    rng = random.Random(2000 + case)
+    hkv = rng.choice([1, 2])
+    hq = hkv * rng.choice([1, 3, 7])
+    d = rng.choice([64, 128])
+    N = rng.choice([2, 3, 4])
+    K = rng.randint(3, 9)
+    lens = [int(min(2500, max(1, rng.lognormvariate(5.0, 1.4)))) for _ in range(K)]
+    lo = max(max(lens) // N + 1, 64)
+    C = rng.randint(lo, max(lo, sum(lens) // N + 256))
+    if planner != "full_shard":
+        C = max(C, -(-sum(lens) // N) + 8)   # round-robin plans one micro-batch: Eq. 10 must hold
+    n_dist, p = _run(lens, hq, hkv, d, N, C, case % 3 != 2, 80 + case, planner=planner)
+    if p is not None and planner == "full_shard":
+        assert n_dist == K
