@@ -124,11 +124,23 @@ struct Bars {
 };
 
 // Steps n = (q-head of the group, query tile); iterated incrementally by every role.
+// SKR_BWD_ORDER 0: q-heads outer, query tiles ascending inner; 1: query tiles ascending outer, the
+// group's q-heads inner (the CTAs in flight stay on nearby query rows for all heads); 2: query tiles
+// DESCENDING outer, heads inner.
+#ifndef SKR_BWD_ORDER
+#define SKR_BWD_ORDER 0
+#endif
 struct StepIter {
-  int hi, qt, qt_first, qt_last;
-  __device__ StepIter(int first, int last) : hi(0), qt(first), qt_first(first), qt_last(last) {}
+  int hi, qt, qt_first, qt_last, grp;
+  __device__ StepIter(int first, int last, int grp_)
+      : hi(0), qt(SKR_BWD_ORDER == 2 ? last : first), qt_first(first), qt_last(last), grp(grp_) {}
   __device__ void next() {
-    if (++qt > qt_last) qt = qt_first, ++hi;
+    if (SKR_BWD_ORDER == 0) {
+      if (++qt > qt_last) qt = qt_first, ++hi;
+    } else if (++hi == grp) {
+      hi = 0;
+      qt += SKR_BWD_ORDER == 2 ? -1 : 1;
+    }
   }
 };
 
@@ -227,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
-    StepIter it(qt_first, qt_last);
+    StepIter it(qt_first, qt_last, grp);
     fetch(it);
     for (int n = 0; n < n_steps; ++n) {
       const int st = n % C::kStages;
@@ -454,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sDS = smem_u32(smem + C::kOffDS);
     const uint32_t sAux = smem_u32(aux);
     const int wg = warp / 4;
-    StepIter it(qt_first, qt_last);
+    StepIter it(qt_first, qt_last, grp);
     // 0 wait Q/dO + S, 1 load S, 2 exp + mask, 3 wait dV done, 4 store P^T, 5 wait dP, 6 dS math, 7 store dS
     PhaseAcct pa;
     pa.start();
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->kt_full);
     }
-    StepIter it(qt_first, qt_last);
+    StepIter it(qt_first, qt_last, grp);
     PhaseAcct pa;   // 0 wait dQ, 1 wait smem tile free, 2 TMEM -> smem, 3 issue reduce
     pa.start();
     for (int n = 0; n < n_steps; ++n, it.next()) {
