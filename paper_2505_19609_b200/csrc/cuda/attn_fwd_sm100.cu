@@ -87,6 +87,11 @@ constexpr int kSoftmax = 256;                // threads per head (two warpgroups
 constexpr int kTmaWarp = 16, kMmaWarp = 17;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
+// softmax warpgroups per head of the d = 128 two-head forward (see attn_fwd_kernel's kWG)
+#ifndef SKR_FWD_WG128
+#define SKR_FWD_WG128 2
+#endif
+
 #ifndef SKR_FWD_BN128
 #define SKR_FWD_BN128 128   // key-tile width of the d = 128 forward (64: separate P columns, see Cfg)
 #endif
@@ -120,15 +125,27 @@ struct Bars {  // kUnits <= 8
   uint64_t q_full;
   uint64_t kv_full[8], kv_empty[8];
   uint64_t s_full[2], s_free[2], p_full[2], pv_done[2];
+  uint64_t p_lo[2];   // kWG = 1: the first kSplitP / 8 of P is in TMEM (split P hand-over)
   uint32_t tmem_base;
 };
 
-template <int D, int kPolyPer8>   // kPolyPer8: exponentials per 8 computed by ex2_poly on the FMA pipe
-__global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers per thread
+// kWG = 1 (d = 128): the PV MMA of a tile is issued in two parts, keys [0, 16 kSplitP) as soon as
+// the softmax has stored that much of P, the rest after the last quarter.
+constexpr int kSplitP = 6;
+
+// kPolyPer8: exponentials per 8 computed by ex2_poly on the FMA pipe.
+// kWG: softmax warpgroups per head. 2: two warpgroups split the key columns of every row and combine
+// their row maxima through shared memory (576 threads, <= 112 registers). 1 (d = 128 only): one
+// warpgroup per head, thread = one full row of S (no cross-warpgroup exchange), P handed to the MMA in
+// two parts (kSplitP) -- 320 threads, <= 200 registers.
+template <int D, int kPolyPer8, int kWG = 2>
+__global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, int pairs_per_group, int head_major) {
   using C = Cfg<D>;
+  static_assert(kWG == 2 || (kWG == 1 && D == 128 && C::kPAlias), "one warpgroup per head: d = 128 only");
+  constexpr int kTmaW = 8 * kWG, kMmaW = 8 * kWG + 1, kSm = 128 * kWG;   // warp roles, softmax threads per head
   const int blk_pair = head_major ? blockIdx.y : blockIdx.x, blk_tile = head_major ? blockIdx.x : blockIdx.y;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -170,20 +187,21 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
     for (int u = 0; u < C::kUnits; ++u) mbar_init(&bars->kv_full[u], 1), mbar_init(&bars->kv_empty[u], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars->s_full[s], 1);
-      mbar_init(&bars->s_free[s], kSoftmax);
-      mbar_init(&bars->p_full[s], kSoftmax);
+      mbar_init(&bars->s_free[s], kSm);
+      mbar_init(&bars->p_full[s], kSm);
       mbar_init(&bars->pv_done[s], 1);
+      mbar_init(&bars->p_lo[s], kSm);
     }
     fence_mbar_init();
   }
   trace_init();
-  if (warp == kMmaWarp) tmem_alloc<512>(&bars->tmem_base);
+  if (warp == kMmaW) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp == kTmaWarp) {
+  if (warp == kTmaW) {
     // ================= TMA producer (warp-converged loop, one elected lane issues)
     if (elect_one()) {
       tma_prefetch_desc(&tm_q);
@@ -220,8 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
       }
     }
     pa.mark(1);
-    if (lane == 0) pa.flush(g_trace_smem, kTmaWarp);
-  } else if (warp == kMmaWarp) {
+    if (lane == 0) pa.flush(g_trace_smem, kTmaW);
+  } else if (warp == kMmaW) {
     // ================= MMA issuer: ONE elected thread runs the whole loop. Measured (profiles/
     // umma_probe.py): the tensor pipe buffers only about one MMA ahead of the issuing thread, and
     // re-entering an elected region per MMA group costs ~200 cycles (R2UR of the descriptors,
@@ -248,6 +266,21 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
           umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
+        umma_commit(&bars->pv_done[s]);
+      };
+      // kWG = 1: PV in two parts, each waiting for its share of P (split hand-over)
+      auto issue_pv_split = [&](int s, int u, bool acc, int jv) {
+        const uint64_t dv = dv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
+        mbar_wait_sleep(&bars->p_lo[s], jv & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kSplitP; ++k)
+          umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
+        mbar_wait_sleep(&bars->p_full[s], jv & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = kSplitP; k < BN / 16; ++k)
+          umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, true);
         umma_commit(&bars->pv_done[s]);
       };
       mbar_wait_sleep(&bars->q_full, 0);
@@ -326,11 +359,17 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
           if (j < n_kv) wait_k(j);
           for (int s = 0; s < nq; ++s) {
             pa.mark(3);
-            mbar_wait_sleep(&bars->p_full[s], jv & 1);
-            pa.mark(2);
-            tc_fence_after();
-            trace(7 + s, jv);
-            issue_pv(s, vunit(jv, s), jv > 0);
+            if (kWG == 2) {
+              mbar_wait_sleep(&bars->p_full[s], jv & 1);
+              pa.mark(2);
+              tc_fence_after();
+              trace(7 + s, jv);
+              issue_pv(s, vunit(jv, s), jv > 0);
+            } else {
+              trace(7 + s, jv);
+              issue_pv_split(s, vunit(jv, s), jv > 0, jv);
+              pa.mark(2);
+            }
             if (j < n_kv) issue_s(s, kunit(j, s));
             trace(3 + s, jv);
           }
@@ -339,9 +378,143 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
         }
       }
       pa.mark(3);
-      pa.flush(g_trace_smem, kMmaWarp);
+      pa.flush(g_trace_smem, kMmaW);
     }
     __syncwarp();
+  } else if constexpr (kWG == 1) {
+    // ================= softmax, one warpgroup per head: head s = warp / 4, thread = query row of the
+    // tile holding all BN key columns (no cross-warpgroup maximum exchange). P (bf16 pairs) goes to
+    // TMEM in four 32-key chunks over S's first columns (already in registers); the MMA starts the
+    // PV of keys [0, 16 kSplitP) after the third chunk (p_lo), the rest after the fourth (p_full).
+    const int s = warp / 4;
+    const int h = s == 0 ? ha : hb;
+    if (h >= 0) {
+      const int row = (warp % 4) * 32 + lane;
+      const uint32_t lane_base = (uint32_t)((warp % 4) * 32) << 16;
+      const uint32_t tS = tmem + lane_base + C::tS(s);
+      const uint32_t tO = tmem + lane_base + C::tO(s);
+      const uint32_t tP = tmem + lane_base + C::tP(s);
+      const int qp = qp0 + row;
+      const float sl2 = a.scale * 1.4426950408889634f;
+      float m_ref = -INFINITY, l = 0.f;
+      PhaseAcct pa;   // 0 wait S, 1 TMEM load S, 2 mask + max, 3 rescale O, 6 exps + store P
+      pa.start();
+      for (int j = 0; j < n_kv; ++j) {
+        mbar_wait(&bars->s_full[s], j & 1);
+        pa.mark(0);
+        tc_fence_after();
+        float x[BN];
+        {
+          uint32_t r[BN / 32][32];
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + 32 * c, r[c]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[32 * c + i] = __uint_as_float(r[c][i]);
+        }
+        pa.mark(1);
+        const int kv0 = j * BN;
+        if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
+#pragma unroll
+          for (int i = 0; i < BN; ++i)
+            if (kv0 + i > qp) x[i] = -INFINITY;
+        }
+        float mxs[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mxs[i] = x[i];
+#pragma unroll
+        for (int i = 8; i < BN; i += 16)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mxs[t] = fmax3(mxs[t], x[i + t], i + 8 + t < BN ? x[i + 8 + t] : x[i + t]);
+        const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                               fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+        const float m_new = fmaxf(m_ref, mx * sl2);
+        // tcgen05.ld/st are warp-collective: the lazy-rescale decision is made per warp
+        const bool rescale = __any_sync(0xffffffffu, m_new > m_ref + kRescaleThreshold) || j == 0;
+        const float alpha = (rescale && j > 0) ? ex2(m_ref - m_new) : 1.f;
+        if (rescale) m_ref = m_new;
+        const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+        pa.mark(2);
+        if (rescale && j > 0) {
+          // O_s must hold every PV up to j - 1 before it is scaled (S_s(j) completed after PV_s(j-1)
+          // in the in-order pipe; the wait makes that explicit), and PV_s(j) only starts after p_lo
+          mbar_wait(&bars->pv_done[s], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(tO + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const float2 v = fmul2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                     make_float2(alpha, alpha));
+              r[i] = __float_as_uint(v.x), r[i + 1] = __float_as_uint(v.y);
+            }
+            tmem_st16(tO + c, r);
+          }
+          tmem_wait_st();
+        }
+        pa.mark(3);
+        float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+#pragma unroll
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            float pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const float2 xx = ffma2(make_float2(x[32 * ch + c + i], x[32 * ch + c + i + 1]), sl2_2, nm2);
+              pv[i] = i < kPolyPer8 ? ex2_poly(xx.x) : ex2(xx.x);
+              pv[i + 1] = i + 1 < kPolyPer8 ? ex2_poly(xx.y) : ex2(xx.y);
+              ls2[(i / 2) % 2] = fadd2(ls2[(i / 2) % 2], make_float2(pv[i], pv[i + 1]));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
+          }
+          tmem_st16(tP + 16 * ch, pk);
+          if (ch == kSplitP / 2 - 1) {          // keys [0, 16 kSplitP) of P are in TMEM
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->p_lo[s]);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full[s]);
+        l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y));
+        pa.mark(6);
+      }
+      if (lane == 0) pa.flush(g_trace_smem, warp);
+      // ---- epilogue: O / l -> bf16 (all D columns of this row), LSE
+      mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+      const bool store = row < n_valid;
+      __nv_bfloat16* orow = out + ((size_t)(r0 + row) * a.hq + h) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tO + c, r);
+        tmem_wait_ld();
+        if (store) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c + i) = v;
+          }
+        }
+      }
+      if (store) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+    }
   } else {
     // ================= softmax: head s = warp / 8, key-column half hf = (warp / 4) % 2
     const int s = warp / 8, hf = (warp / 4) % 2;
@@ -398,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
         float* rj = red + (j & 1) * (2 * BM);
         rj[hf * BM + row] = mx;
         tc_fence_before();                    // (d = 128) this half's S loads precede the partner's P stores
-        named_bar_sync(1 + s, kSoftmax);
+        named_bar_sync(1 + s, kSm);
         tc_fence_after();
         mx = fmaxf(mx, rj[(1 - hf) * BM + row]);
         const float m_new = fmaxf(m_ref, mx * sl2);
@@ -460,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
       // ---- epilogue: combine the halves' row sums, O / l -> bf16 (this half's d columns), LSE
       float* lr = red + (n_kv & 1) * (2 * BM);   // a parity slot no half reads any more
       lr[hf * BM + row] = l;
-      named_bar_sync(1 + s, kSoftmax);
+      named_bar_sync(1 + s, kSm);
       l += lr[(1 - hf) * BM + row];
       mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
       tc_fence_after();
@@ -486,10 +659,10 @@ __global__ void __launch_bounds__(kThreads, 1)   // 18 warps -> <= 112 registers
       }
       if (store && hf == 0) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
     }
-  }
+    }
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+  if (warp == kMmaW) tmem_dealloc<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1077,9 +1250,9 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   // measured (profiles/fwd_period.py, S = 32K): d=64 best at 2/8, d=128 at 1/8; beyond that the
   // polynomial's FMA / ALU instructions cost more issue slots than the MUFU time they save
   const int pp = poly >= 0 ? poly : (d == 64 ? 2 : 1);
-  auto launch = [&](auto kern, int smem) {
+  auto launch = [&](auto kern, int smem, int threads = fwd::kThreads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<grid, fwd::kThreads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg, head_major);
+    kern<<<grid, threads, smem, st>>>(tq, tk, tv, a, (__nv_bfloat16*)o, lse, ppg, head_major);
   };
   // d = 128, one head per CTA (double-buffered S, separate P): opt-in, SKR_FWD_1H=1 (measured slower:
   // without the GQA head pair each K/V tile is loaded and read per head, profiles/r01_experiments.md)
@@ -1117,6 +1290,14 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
   }
   if (d == 128) {
     constexpr int smem = fwd::Cfg<128>::kSmem;
+#if SKR_FWD_WG128 == 1
+    constexpr int t1 = (8 * 1 + 2) * 32;   // one softmax warpgroup per head
+    switch (pp) {
+      case 0: launch(fwd::attn_fwd_kernel<128, 0, 1>, smem, t1); break;
+      case 1: launch(fwd::attn_fwd_kernel<128, 1, 1>, smem, t1); break;
+      default: launch(fwd::attn_fwd_kernel<128, 2, 1>, smem, t1); break;
+    }
+#else
     switch (pp) {
       case 0: launch(fwd::attn_fwd_kernel<128, 0>, smem); break;
       case 1: launch(fwd::attn_fwd_kernel<128, 1>, smem); break;
@@ -1124,6 +1305,7 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
       case 3: launch(fwd::attn_fwd_kernel<128, 3>, smem); break;
       default: launch(fwd::attn_fwd_kernel<128, 4>, smem); break;
     }
+#endif
   } else if (d == 64) {
     constexpr int smem = fwd::Cfg<64>::kSmem;
     switch (pp) {

@@ -27,14 +27,18 @@ for _ in range(3):
     sk.skr_attn_fwd(shape, fs, q, k, v, o, lse)
     torch.cuda.synchronize()
 sk._lib.skr_debug_fwd_trace(buf, 8192)
-a = np.array(buf[:144], dtype=np.int64).reshape(18, 8)
+WG = int(os.environ.get("SKR_FWD_WG", "2"))   # softmax warpgroups per head of the build (kWG)
+NW = 8 * WG + 2
+a = np.array(buf[:NW * 8], dtype=np.int64).reshape(NW, 8)
 n_kv = S // 128   # block (0, 0) runs the LPT-first (longest) q tile
-names = {"sm": ["wait S", "ld S", "max+xchg", "wait PV", "store P", "-", "exps"], 16: ["wait slot", "issue"],
-         17: ["wait K", "wait V", "wait S/P", "issue"]}
+names = {"sm": ["wait S", "ld S", "max+xchg", "wait PV", "store P", "-", "exps"] if WG == 2 else
+         ["wait S", "ld S", "mask+max", "rescale O", "-", "-", "exps+st P"],
+         NW - 2: ["wait slot", "issue"], NW - 1: ["wait K", "wait V", "wait S/P", "issue"]}
 print(f"d={d} S={S}: cycles per KV tile (n_kv={n_kv})")
-for w in range(18):
-    lab = names["sm"] if w < 16 else names[w]
+for w in range(NW):
+    lab = names["sm"] if w < NW - 2 else names[w]
     row = "  ".join(f"{lab[i]} {a[w, i] / n_kv:7.0f}" for i in range(len(lab)))
     tot = a[w, :len(lab)].sum() / n_kv
-    who = f"{'A' if w < 8 else 'B'}{(w // 4) % 2} w{w % 4}" if w < 16 else ("TMA" if w == 16 else "MMA")
+    who = (f"{'A' if w < 4 * WG else 'B'}{(w // 4) % WG} w{w % 4}" if w < NW - 2 else
+           ("TMA" if w == NW - 2 else "MMA"))
     print(f"{who:5s} total {tot:7.0f} | {row}")
