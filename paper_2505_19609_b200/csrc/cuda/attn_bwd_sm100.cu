@@ -545,9 +545,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int b = 0; b < kBatch; ++b) tmem_ld32(tmem + lane_base + C::tDP + col0 + cb + 32 * b, r[b]);
           tmem_wait_ld();
-          if (cb + 32 * kBatch >= H) {
+          if (!C::kDSAlias && cb + 32 * kBatch >= H) {
+            // dP TMEM may be overwritten by dP(n+1). (d = 64: dS^T aliases dP^T, so dP(n+1) is
+            // ordered after this step's ds_full instead and dp_free is not used -- an arrive nobody
+            // waits for is what compute-sanitizer's synccheck flagged)
             tc_fence_before();
-            mbar_arrive(&bars->dp_free);            // dP TMEM may be overwritten by dP(n+1)
+            mbar_arrive(&bars->dp_free);
           }
 #pragma unroll
           for (int b = 0; b < kBatch; ++b)
