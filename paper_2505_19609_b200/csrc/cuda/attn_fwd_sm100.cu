@@ -91,6 +91,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef SKR_FWD_WG128
 #define SKR_FWD_WG128 2
 #endif
+#ifndef SKR_FWD_WG64
+#define SKR_FWD_WG64 2
+#endif
 
 #ifndef SKR_FWD_BN128
 #define SKR_FWD_BN128 128   // key-tile width of the d = 128 forward (64: separate P columns, see Cfg)
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
                     const __grid_constant__ CUtensorMap tm_v, AttnArgs a, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, int pairs_per_group, int head_major) {
   using C = Cfg<D>;
-  static_assert(kWG == 2 || (kWG == 1 && D == 128 && C::kPAlias), "one warpgroup per head: d = 128 only");
+  static_assert(kWG == 2 || (kWG == 1 && C::BN == 128), "one warpgroup per head: 128-key tiles");
   constexpr int kTmaW = 8 * kWG, kMmaW = 8 * kWG + 1, kSm = 128 * kWG;   // warp roles, softmax threads per head
   const int blk_pair = head_major ? blockIdx.y : blockIdx.x, blk_tile = head_major ? blockIdx.x : blockIdx.y;
   constexpr int BN = C::BN;
@@ -338,11 +341,16 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
             wait_v(jv);
             for (int s = 0; s < nq; ++s) {
               pa.mark(3);
-              mbar_wait_sleep(&bars->p_full[s], jv & 1);
-              pa.mark(2);
-              tc_fence_after();
               trace(7 + s, jv);
-              issue_pv(s, vunit(jv, s), jv > 0);
+              if (kWG == 2) {
+                mbar_wait_sleep(&bars->p_full[s], jv & 1);
+                pa.mark(2);
+                tc_fence_after();
+                issue_pv(s, vunit(jv, s), jv > 0);
+              } else {
+                issue_pv_split(s, vunit(jv, s), jv > 0, jv);
+                pa.mark(2);
+              }
               trace(3 + s, jv);
             }
             free_v(jv);
@@ -384,8 +392,10 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
   } else if constexpr (kWG == 1) {
     // ================= softmax, one warpgroup per head: head s = warp / 4, thread = query row of the
     // tile holding all BN key columns (no cross-warpgroup maximum exchange). P (bf16 pairs) goes to
-    // TMEM in four 32-key chunks over S's first columns (already in registers); the MMA starts the
-    // PV of keys [0, 16 kSplitP) after the third chunk (p_lo), the rest after the fourth (p_full).
+    // TMEM in four 32-key chunks; the MMA starts the PV of keys [0, 16 kSplitP) after the third
+    // chunk (p_lo), the rest after the fourth (p_full). d = 128: P aliases S's first columns (already
+    // in registers). d = 64: P has its own columns, so S_s(j+1) may be issued as soon as S_s(j) is
+    // loaded (s_free), and P_s(j) is written only after PV_s(j-1) has read P_s(j-1).
     const int s = warp / 4;
     const int h = s == 0 ? ha : hb;
     if (h >= 0) {
@@ -414,6 +424,10 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[32 * c + i] = __uint_as_float(r[c][i]);
         }
+        if (!C::kPAlias) {
+          tc_fence_before();
+          mbar_arrive(&bars->s_free[s]);      // S_s TMEM may now take S_s(j+1)
+        }
         pa.mark(1);
         const int kv0 = j * BN;
         if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
@@ -437,6 +451,64 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         if (rescale) m_ref = m_new;
         const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
         pa.mark(2);
+        float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+        if (!C::kPAlias) {
+          // exponentials first (registers: P packed, 64 words); P / O only after PV_s(j-1)
+          uint32_t pk[BN / 2];
+#pragma unroll
+          for (int c = 0; c < BN; c += 8) {
+            float pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const float2 xx = ffma2(make_float2(x[c + i], x[c + i + 1]), sl2_2, nm2);
+              pv[i] = i < kPolyPer8 ? ex2_poly(xx.x) : ex2(xx.x);
+              pv[i + 1] = i + 1 < kPolyPer8 ? ex2_poly(xx.y) : ex2(xx.y);
+              ls2[(i / 2) % 2] = fadd2(ls2[(i / 2) % 2], make_float2(pv[i], pv[i + 1]));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf16(pv[2 * i], pv[2 * i + 1]);
+          }
+          pa.mark(6);
+          if (j > 0) {
+            mbar_wait(&bars->pv_done[s], (j - 1) & 1);
+            tc_fence_after();
+          }
+          if (rescale && j > 0) {
+#pragma unroll
+            for (int c = 0; c < D; c += 16) {
+              uint32_t r[16];
+              tmem_ld16(tO + c, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; i += 2) {
+                const float2 v = fmul2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                       make_float2(alpha, alpha));
+                r[i] = __float_as_uint(v.x), r[i + 1] = __float_as_uint(v.y);
+              }
+              tmem_st16(tO + c, r);
+            }
+          }
+          pa.mark(3);
+#pragma unroll
+          for (int ch = 0; ch < BN / 32; ++ch) {
+            uint32_t q16[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) q16[i] = pk[16 * ch + i];
+            tmem_st16(tP + 16 * ch, q16);
+            if (ch == kSplitP / 2 - 1) {
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&bars->p_lo[s]);
+            }
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bars->p_full[s]);
+          l = (rescale ? (j == 0 ? 0.f : l * alpha) : l) + ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y));
+          pa.mark(4);
+          continue;
+        }
         if (rescale && j > 0) {
           // O_s must hold every PV up to j - 1 before it is scaled (S_s(j) completed after PV_s(j-1)
           // in the in-order pipe; the wait makes that explicit), and PV_s(j) only starts after p_lo
@@ -458,8 +530,6 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
           tmem_wait_st();
         }
         pa.mark(3);
-        float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        const float2 sl2_2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
 #pragma unroll
         for (int ch = 0; ch < BN / 32; ++ch) {
           uint32_t pk[16];
@@ -1308,6 +1378,16 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
 #endif
   } else if (d == 64) {
     constexpr int smem = fwd::Cfg<64>::kSmem;
+#if SKR_FWD_WG64 == 1
+    constexpr int t1 = (8 * 1 + 2) * 32;   // one softmax warpgroup per head
+    switch (pp) {
+      case 0: launch(fwd::attn_fwd_kernel<64, 0, 1>, smem, t1); break;
+      case 1: launch(fwd::attn_fwd_kernel<64, 1, 1>, smem, t1); break;
+      case 2: launch(fwd::attn_fwd_kernel<64, 2, 1>, smem, t1); break;
+      default: launch(fwd::attn_fwd_kernel<64, 3, 1>, smem, t1); break;
+    }
+    return launch_status("attn_fwd_kernel");
+#endif
     switch (pp) {
       case 0: launch(fwd::attn_fwd_kernel<64, 0>, smem); break;
       case 1: launch(fwd::attn_fwd_kernel<64, 1>, smem); break;
