@@ -62,8 +62,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="workload (default: C2, weak-scaled by N)")
     ap.add_argument("--dp", type=int, default=1, help="DP degree of the DP x CP grid (CP = N / dp)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
-                    help="CP exchange: NCCL all-gather / reduce-scatter, or the peer-memory kernels (row f3)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "peer1"],
+                    help="CP exchange: NCCL all-gather / reduce-scatter; 'peer': row f3 step two (peer gather, "
+                         "dK/dV reduced from the backward kernel's epilogue into the owners' memory); 'peer1': "
+                         "row f3 step one (peer gather + peer-reduce pass)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -324,11 +326,11 @@ def run_ours(args):
     if cp > 1:
         # one communicator per CP group (every rank takes part in creating every group)
         groups = [dist.new_group(list(range(d * cp, (d + 1) * cp))) for d in range(dp)]
-        if args.exchange == "peer":
+        if args.exchange in ("peer", "peer1"):
             comm = sk.PeerComm(cp, cp_rank, group=groups[dp_rank])
         else:
             comm = sk.Comm(cp, cp_rank, group=groups[dp_rank], src=dp_rank * cp)
-    nccl_comm = comm if (comm is not None and args.exchange != "peer") else None
+    nccl_comm = comm if (comm is not None and args.exchange == "nccl") else None
     side = torch.cuda.Stream(priority=-1)
     main = torch.cuda.current_stream()
     steps = []
@@ -340,7 +342,7 @@ def run_ours(args):
     for rs in rsteps:
         rs.rebind(pool.get)
     for j, rs in enumerate(rsteps):
-        if args.exchange == "peer" and comm is not None:
+        if args.exchange in ("peer", "peer1") and comm is not None:
             rs.connect_peer(comm)              # collective inside the CP group
         g.manual_seed(args.seed * 1_000_003 + rank * 1009 + j)
         R = max(rs.rows, 1)
@@ -350,11 +352,11 @@ def run_ours(args):
 
     def fwd_bwd(rs, src, ev_do=None, timing=None):
         # ev_do (e2e only): the backward waits for this micro-batch's dO copy, the forward does not
-        if args.exchange == "peer" and comm is not None:
+        if args.exchange in ("peer", "peer1") and comm is not None:
             rs.forward_peer(src["q"], src["k"], src["v"], side)
             if ev_do is not None:
                 torch.cuda.current_stream().wait_event(ev_do)
-            rs.backward_peer(src["do"], side)
+            (rs.backward_peer_fused if args.exchange == "peer" else rs.backward_peer)(src["do"], side)
         else:
             rs.forward(src["q"], src["k"], src["v"], comm, side, timing=timing)
             if ev_do is not None:
@@ -383,7 +385,7 @@ def run_ours(args):
         if nccl_comm is not None:
             nccl_comm.wait(main, timeout_s=600.0)
         torch.cuda.synchronize()
-        if comm is not None and args.exchange == "peer":
+        if comm is not None and args.exchange in ("peer", "peer1"):
             comm.check()
 
     def barrier():
@@ -398,7 +400,7 @@ def run_ours(args):
     # per-(step, micro-batch) attention timing events (recorded by the library inside the composite
     # steps); created up front so recording them costs nothing in the loop
     K = args.steps
-    use_lib_timing = not (args.exchange == "peer" and comm is not None)
+    use_lib_timing = not (args.exchange in ("peer", "peer1") and comm is not None)
     timing = None
     if use_lib_timing:
         timing = [[[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(n_mb)] for _ in range(K)]

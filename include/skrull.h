@@ -228,6 +228,27 @@ skr_status skr_peer_gather_chunks(const uint64_t* peer_packed, const int32_t* ch
 skr_status skr_peer_reduce_chunks(const uint64_t* peer_partials, int32_t nranks, int32_t rank,
                                   const int32_t* chunk_table, int32_t n_chunks, int32_t row_elems,
                                   int32_t pad_rows_P, void* dst, int32_t dst_bf16, void* stream);
+/* Row f3, step two: the a9 reduction fused into the backward of the DISTRIBUTED chunks (a8), so the
+ * tensor-core kernel itself performs the collective's data movement: every dK / dV fp32 partial row
+ * the kernel produces is red-added (red.global.add.f32, peer stores over NVLink) straight into the
+ * accumulator of the rank that OWNS that key row -- no local partial buffer, no permute, no
+ * reduce-scatter, no peer-reduce pass. Arguments as skr_attn_bwd for the distributed segment class
+ * (k, v = the natural distributed K / V buffer, dq as there), plus:
+ *   peer_dk, peer_dv : device arrays [nranks] of the ranks' fp32 accumulators [pad_rows_P][hkv][d]
+ *                      (row r = row r of the owner's distributed prefix), zeroed by their owners and
+ *                      made visible (epoch flags) before the launch;
+ *   row_map          : device int32 [natural rows]: natural row -> owner * pad_rows_P + prefix row
+ *                      (skr_pack_owner_rows).
+ * The owner casts its accumulator rows [0, dist_rows) into its packed bf16 dK / dV prefix after every
+ * rank's kernel has completed (epoch flags). fp32 test mode: the same with atomicAdd. */
+skr_status skr_attn_bwd_peer(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k, const void* v,
+                             const void* o, const void* dout, const float* lse, void* dq, const uint64_t* peer_dk,
+                             const uint64_t* peer_dv, const int32_t* row_map, int32_t pad_rows_P, int32_t n_q_rows,
+                             int32_t n_kv_rows, void* ws, size_t ws_bytes, void* stream);
+/* Host: row_map for skr_attn_bwd_peer from skr_pack_chunks' table: for every chunk row and r < len,
+ * row_map[natural_row + r] = gathered_row + r (= owner * P + row in the owner's distributed prefix).
+ * row_map has natural_rows entries; SKR_E_ARG if a chunk row falls outside it. */
+skr_status skr_pack_owner_rows(const int32_t* chunk_table, int32_t n_chunks, int32_t natural_rows, int32_t* row_map);
 /* Epoch flags (uint32 per rank): signal stores `epoch` into slot `rank` of every peer's flag array
  * (system-scope release after a system fence, ordered after this stream's earlier work); wait
  * blocks the stream until every slot of this rank's flags reached `epoch`, or sets *err = 1 after

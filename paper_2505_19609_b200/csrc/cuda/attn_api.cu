@@ -73,10 +73,37 @@ SKR_EXPORT skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, c
   return sm100_attn_fwd(a, s->d, q, k, v, o, lse, n_q_rows, n_kv_rows, st);
 }
 
+static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
+                                const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
+                                void* dv, int32_t kv_accumulate, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
+                                size_t ws_bytes, void* stream, const uint64_t* peer_dk, const uint64_t* peer_dv,
+                                const int32_t* row_map, int32_t pad_P);
+
 SKR_EXPORT skr_status skr_attn_bwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
                                    const void* v, const void* o, const void* dout, const float* lse, void* dq,
                                    void* dk, void* dv, int32_t kv_accumulate, int32_t n_q_rows, int32_t n_kv_rows,
                                    void* ws, size_t ws_bytes, void* stream) {
+  SKR_REQUIRE(kv_accumulate == 0 || kv_accumulate == 1, "skr_attn_bwd: kv_accumulate must be 0 or 1");
+  return attn_bwd_impl(s, g, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate, n_q_rows, n_kv_rows, ws, ws_bytes,
+                       stream, nullptr, nullptr, nullptr, 0);
+}
+
+SKR_EXPORT skr_status skr_attn_bwd_peer(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
+                                        const void* v, const void* o, const void* dout, const float* lse, void* dq,
+                                        const uint64_t* peer_dk, const uint64_t* peer_dv, const int32_t* row_map,
+                                        int32_t pad_rows_P, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
+                                        size_t ws_bytes, void* stream) {
+  SKR_REQUIRE(peer_dk && peer_dv && row_map && pad_rows_P > 0, "skr_attn_bwd_peer: null peer table / P = 0");
+  // dk / dv are unused in this mode; pass the peer tables so the null checks hold
+  return attn_bwd_impl(s, g, q, k, v, o, dout, lse, dq, (void*)peer_dk, (void*)peer_dv, 2, n_q_rows, n_kv_rows, ws,
+                       ws_bytes, stream, peer_dk, peer_dv, row_map, pad_rows_P);
+}
+
+static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
+                                const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
+                                void* dv, int32_t kv_accumulate, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
+                                size_t ws_bytes, void* stream, const uint64_t* peer_dk, const uint64_t* peer_dv,
+                                const int32_t* row_map, int32_t pad_P) {
   if (skr_status e = check_shape(s)) return e;
   SKR_REQUIRE(g && n_q_rows >= 0 && n_kv_rows >= 0, "skr_attn_bwd: bad segments / sizes");
   SKR_REQUIRE(g->row_begin >= 0 && g->row_begin <= g->row_end && g->row_end <= n_q_rows,
@@ -89,6 +116,10 @@ SKR_EXPORT skr_status skr_attn_bwd(const skr_attn_shape* s, const skr_segs* g, c
   if (ws_bytes < need) return fail(SKR_E_CAPACITY, "skr_attn_bwd: workspace %zu < %zu bytes", ws_bytes, need);
   if (skr_status e = check_sm100()) return e;
   AttnArgs a = make_args(s, g, n_q_rows);
+  a.peer_dk = peer_dk;
+  a.peer_dv = peer_dv;
+  a.row_map = row_map;
+  a.pad_P = pad_P;
   cudaStream_t st = (cudaStream_t)stream;
   float* Dbuf = (float*)ws;
   if (s->dtype == SKR_FP32) {

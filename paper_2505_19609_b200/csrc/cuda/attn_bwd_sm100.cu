@@ -599,6 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool valid = kvp < k_len;
     const size_t row = (size_t)(kst + kvp) * a.hkv + g;
     const int which = warp / 4;
+    // accumulate == 2: this key row's partial goes to its owner's accumulator (peer memory)
+    float* const peer = (accumulate == 2 && valid) ? peer_row(a, which == 0, kst + kvp) + (size_t)g * D : nullptr;
     const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
     const float mul = which == 0 ? a.scale : 1.f;
 #pragma unroll
@@ -608,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       if (!valid) continue;
       if (accumulate) {
-        float* dst = reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D + c;
+        float* dst = accumulate == 2 ? peer + c : reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D + c;
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
           red_add_v4(dst + i, __uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul,

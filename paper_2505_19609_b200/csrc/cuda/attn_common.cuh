@@ -17,7 +17,21 @@ struct AttnArgs {
   int hq, hkv;
   float scale;
   int ld_lse;              // row stride of lse / D buffers ([h][ld_lse])
+  // backward with kv_accumulate == 2 (row f3, fused peer reduction): dK / dV fp32 partials are
+  // red-added straight into each key row's OWNER accumulator: owner = row_map[k] / pad_P, row
+  // row_map[k] % pad_P of the [pad_P][hkv][d] fp32 buffers at peer_dk[owner] / peer_dv[owner]
+  const uint64_t* peer_dk = nullptr;
+  const uint64_t* peer_dv = nullptr;
+  const int32_t* row_map = nullptr;   // [natural K rows] -> owner * pad_P + row in the owner's prefix
+  int pad_P = 0;
 };
+
+// destination row of a dK / dV partial in accumulate mode 2 (see AttnArgs)
+__device__ __forceinline__ float* peer_row(const AttnArgs& a, bool is_dk, int krow) {
+  const int gr = a.row_map[krow];
+  const int owner = gr / a.pad_P, prow = gr - owner * a.pad_P;
+  return reinterpret_cast<float*>(is_dk ? a.peer_dk[owner] : a.peer_dv[owner]) + (size_t)prow * a.hkv;
+}
 
 skr_status simt_attn_fwd(const AttnArgs& a, int d, const float* q, const float* k, const float* v, float* o,
                          float* lse, cudaStream_t st);

@@ -14,6 +14,7 @@
 //   main : attention bwd over LOCAL segments (overlaps the exchange); wait ev_rs
 // With no distributed sequence no collective is issued (T_comm(0) = 0, R26) and comm may be null.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: named ranges for nsys / ncu --nvtx (SURVEY §5 tracing)
 
 #include "attn_common.cuh"
 #include "device.cuh"
@@ -63,6 +64,13 @@ skr_status mark(const skr_cp_step* st, int i, cudaStream_t m) {
   return skr::cuda_status(cudaEventRecord((cudaEvent_t)st->timing_events[i], m), "record timing event");
 }
 
+// NVTX range scoped to a C-ABI phase (host-side markers around the enqueue of each row's work;
+// free when no tool is attached)
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
+
 size_t row_bytes(const skr_attn_shape& s, int heads) {
   return (size_t)heads * s.d * (s.dtype == SKR_FP32 ? 4 : 2);
 }
@@ -83,16 +91,19 @@ SKR_EXPORT void skr_attn_plan_destroy(skr_attn_plan* p) { delete p; }
 SKR_EXPORT skr_status skr_cp_attn_fwd(skr_comm* comm, const skr_attn_plan* plan, const skr_cp_step* st, void* main,
                                       void* side) {
   if (skr_status e = check_step(plan, st, comm, "skr_cp_attn_fwd")) return e;
+  Range r_all("skr_cp_attn_fwd");
   const skr_attn_shape& s = plan->shape;
   const bool dist = st->natural_rows > 0;
   cudaStream_t m = (cudaStream_t)main, sd = (cudaStream_t)side;
   Events& ev = events();
   if (st->rows) {   // a5
+    Range r("a5 pack Q/K/V");
     if (skr_status e = skr_pack_rows(st->q_src, st->src_row, st->rows, (int32_t)row_bytes(s, s.hq), st->q, m)) return e;
     if (skr_status e = skr_pack_rows(st->k_src, st->src_row, st->rows, (int32_t)row_bytes(s, s.hkv), st->k, m)) return e;
     if (skr_status e = skr_pack_rows(st->v_src, st->src_row, st->rows, (int32_t)row_bytes(s, s.hkv), st->v, m)) return e;
   }
   if (dist) {       // a6 on the side stream
+    Range r("a6 all-gather + reorder (side stream)");
     const size_t kvb = row_bytes(s, s.hkv);
     if (skr_status e = cuda_status(cudaEventRecord(ev.a, m), "record packed")) return e;
     if (skr_status e = cuda_status(cudaStreamWaitEvent(sd, ev.a, 0), "wait packed")) return e;
@@ -109,6 +120,7 @@ SKR_EXPORT skr_status skr_cp_attn_fwd(skr_comm* comm, const skr_attn_plan* plan,
     if (skr_status e = cuda_status(cudaEventRecord(ev.b, sd), "record kv")) return e;
   }
   // a7: locals first (they need no exchange), then the distributed chunks
+  Range r7("a7 attention fwd");
   if (skr_status e = mark(st, 0, m)) return e;
   if (skr_status e = skr_attn_fwd(&s, &st->local_fwd, st->q, st->k, st->v, st->o, st->lse, st->buf_rows, st->buf_rows, m))
     return e;
@@ -128,6 +140,7 @@ SKR_EXPORT skr_status skr_cp_attn_fwd(skr_comm* comm, const skr_attn_plan* plan,
 SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan, const skr_cp_step* st, void* main,
                                       void* side) {
   if (skr_status e = check_step(plan, st, comm, "skr_cp_attn_bwd")) return e;
+  Range r_all("skr_cp_attn_bwd");
   const skr_attn_shape& s = plan->shape;
   const bool dist = st->natural_rows > 0;
   cudaStream_t m = (cudaStream_t)main, sd = (cudaStream_t)side;
@@ -143,6 +156,7 @@ SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan,
   }
   if (skr_status e = mark(st, 4, m)) return e;
   if (dist) {
+    Range r("a8 attention bwd, distributed chunks");
     if (skr_status e = skr_attn_bwd(&s, &st->dist_bwd, st->q, st->k_natural, st->v_natural, st->o, st->dout, st->lse,
                                     st->dq, st->dk_partial, st->dv_partial, 1, st->buf_rows, st->natural_rows, st->ws,
                                     st->ws_bytes, m))
@@ -150,6 +164,7 @@ SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan,
   }
   if (skr_status e = mark(st, 5, m)) return e;
   if (dist) {
+    Range r("a9 permute + reduce-scatter + cast (side stream)");
     if (skr_status e = cuda_status(cudaEventRecord(ev.a, m), "record partials")) return e;
     if (skr_status e = cuda_status(cudaStreamWaitEvent(sd, ev.a, 0), "wait partials")) return e;
     const int32_t f32b = (int32_t)((size_t)s.hkv * s.d * 4);
@@ -182,6 +197,7 @@ SKR_EXPORT skr_status skr_cp_attn_bwd(skr_comm* comm, const skr_attn_plan* plan,
     }
     if (skr_status e = cuda_status(cudaEventRecord(ev.b, sd), "record rs")) return e;
   }
+  Range r8("a8 attention bwd, local segments");
   if (skr_status e = mark(st, 6, m)) return e;
   if (skr_status e = skr_attn_bwd(&s, &st->local_bwd, st->q, st->k, st->v, st->o, st->dout, st->lse, st->dq, st->dk,
                                   st->dv, 0, st->buf_rows, st->buf_rows, st->ws, st->ws_bytes, m))

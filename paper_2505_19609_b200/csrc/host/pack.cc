@@ -229,3 +229,20 @@ SKR_EXPORT skr_status skr_tiles_bwd(const int32_t* cu, const int32_t* q_pos, con
   }
   return emit_tiles(v, tiles, cap, n_tiles);
 }
+
+SKR_EXPORT skr_status skr_pack_owner_rows(const int32_t* table, int32_t n_chunks, int32_t natural_rows,
+                                          int32_t* row_map) {
+  SKR_REQUIRE(n_chunks >= 0 && natural_rows >= 0 && (n_chunks == 0 || table) && (natural_rows == 0 || row_map),
+              "skr_pack_owner_rows: bad arguments");
+  for (int32_t i = 0; i < natural_rows; ++i) row_map[i] = -1;
+  for (int32_t c = 0; c < n_chunks; ++c) {
+    const int32_t* t = table + 6 * c;
+    const int64_t g = t[3], n = t[4], len = t[5];
+    SKR_REQUIRE(len >= 0 && n >= 0 && n + len <= natural_rows && g >= 0 && g + len <= INT32_MAX,
+                "skr_pack_owner_rows: chunk %d outside the natural rows", c);
+    for (int64_t r = 0; r < len; ++r) row_map[n + r] = (int32_t)(g + r);
+  }
+  for (int32_t i = 0; i < natural_rows; ++i)
+    SKR_REQUIRE(row_map[i] >= 0, "skr_pack_owner_rows: natural row %d has no chunk", i);
+  return SKR_OK;
+}

@@ -91,7 +91,10 @@ class RankStep:
         self.loc_f = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "fwd", device)
         self.loc_b = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "bwd", device)
         if self.has_dist:
-            self.chunks = torch.as_tensor(sk.skr_pack_chunks(mb_lens, assign, cp).reshape(-1)).to(device)
+            table = sk.skr_pack_chunks(mb_lens, assign, cp)
+            self.chunks = torch.as_tensor(table.reshape(-1)).to(device)
+            # row f3 step two: natural row -> owner * P + prefix row (skr_attn_bwd_peer)
+            self.owner_rows = torch.as_tensor(sk.skr_pack_owner_rows(table, self.nat_rows)).to(device)
         # packed buffers (>= P rows so the all-gather send prefix is always in bounds)
         R = max(self.rows, self.P, 1)
         f32, dt = torch.float32, self.dt
@@ -113,6 +116,10 @@ class RankStep:
                 self._buf(name, (N * P, hkv, d), f32)
             for name in ("dk_red", "dv_red"):
                 self._buf(name, (P, hkv, d), f32)
+            # row f3 step two: this rank's fp32 accumulators of the rows it OWNS (its distributed
+            # prefix); every rank's backward red-adds its partials into them over peer memory
+            for name in ("dk_acc", "dv_acc"):
+                self._buf(name, (max(P, 1), hkv, d), f32)
 
     def cp_step(self, q_src, k_src, v_src, do_src, timing=None):
         """The skr_cp_step of this micro-batch (row a5-a9 composite C-ABI call) for these inputs.
@@ -162,7 +169,10 @@ class RankStep:
             dist_rows = self.dist_b.row_end - self.dist_b.row_begin
             n += (self.dist_f.n_tiles > 0) + (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)
             if exchange == "peer":
-                n += 2 + 2 + 3 * 2                            # gather K, V; reduce dK, dV; 3 signal+wait
+                # step two: gather K, V; cast dK, dV (the reduction is inside the bwd kernel); 3 signal + wait
+                n += 2 + 2 * (self.dist_rows > 0) + 3 * 2
+            elif exchange == "peer1":
+                n += 2 + 2 + 3 * 2                            # gather K, V; reduce dK, dV; 3 signal + wait
             else:
                 n += 2 + 2 + 2 * (self.dist_rows > 0)         # reorder K, V; scatter dK, dV; cast dK, dV
         return n
@@ -296,11 +306,12 @@ class RankStep:
 
     # ------------------------------------------------------------------ row f3: peer-memory exchange
     def connect_peer(self, peer):
-        """Collective over the CP group: map the peers' packed K/V and natural fp32 dK/dV partials."""
+        """Collective over the CP group: map the peers' packed K/V, natural fp32 dK/dV partials (step
+        one) and owned fp32 dK/dV accumulators (step two)."""
         self.peer = peer
         if self.has_dist:
-            self.peer_k, self.peer_v, self.peer_dk, self.peer_dv = peer.exchange(
-                [self.k, self.v, self.dk_nat, self.dv_nat])
+            self.peer_k, self.peer_v, self.peer_dk, self.peer_dv, self.peer_dk_acc, self.peer_dv_acc = peer.exchange(
+                [self.k, self.v, self.dk_nat, self.dv_nat, self.dk_acc, self.dv_acc])
 
     def peer_gather(self, stream=None):
         sk.skr_peer_gather_chunks(self.peer_k, self.chunks, self.n_chunks, self.P, self.k_nat, stream)
@@ -312,6 +323,57 @@ class RankStep:
                                   self.dk, stream)
         sk.skr_peer_reduce_chunks(self.peer_dv, self.cp, self.rank, self.chunks, self.n_chunks, re, self.P,
                                   self.dv, stream)
+
+    def bwd_dist_fused(self, stream=None):
+        """Row f3 step two: the distributed chunks' backward red-adds its dK/dV partials straight into
+        the OWNERS' fp32 accumulators (peer memory) from the kernel epilogue."""
+        self._timed("bwd_dist", lambda: sk.skr_attn_bwd_peer(
+            self.shape, self.dist_b, self.q, self.k_nat, self.v_nat, self.o, self.do, self.lse, self.dq,
+            self.peer_dk_acc, self.peer_dv_acc, self.owner_rows, self.P, self.ws, stream), stream)
+
+    def acc_zero(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.dk_acc.zero_()
+            self.dv_acc.zero_()
+
+    def acc_cast(self, stream=None):
+        """Owner side: the summed fp32 rows of this rank's distributed prefix -> packed dK/dV."""
+        n = self.dist_rows
+        if n:
+            if self.dt == torch.float32:
+                s = stream if stream is not None else torch.cuda.current_stream()
+                with torch.cuda.stream(s):
+                    self.dk[:n].copy_(self.dk_acc[:n])
+                    self.dv[:n].copy_(self.dv_acc[:n])
+            else:
+                sk.skr_cast_f32_bf16(self.dk_acc[:n], self.dk[:n], stream)
+                sk.skr_cast_f32_bf16(self.dv_acc[:n], self.dv[:n], stream)
+
+    def backward_peer_fused(self, do_src, side):
+        """Mirror of Eq. 2 (R24) with the a9 exchange fused into the a8 kernel (row f3 step two):
+        main: pack dO; zero the owned accumulators; epoch 'zeroed' (all ranks); distributed backward
+        (red-adds into the owners' accumulators over NVLink); epoch 'added'; side: wait for every
+        rank's 'added', cast the owned rows into the packed bf16 dK/dV prefix, while main runs the
+        local tiles. A rank zeroes its accumulators for the next micro-batch only after its cast
+        (main waits for the side stream), and the others add into them only after the next
+        'zeroed' epoch, so no extra 'consumed' epoch is needed."""
+        main = torch.cuda.current_stream()
+        self.pack_do(do_src)
+        if self.has_dist:
+            self.acc_zero(main)
+            e = self.peer.signal(main)
+            self.peer.wait(e, main)
+            self.bwd_dist_fused()
+            e2 = self.peer.signal(main)
+            with torch.cuda.stream(side):
+                self.peer.wait(e2, side)
+                self.acc_cast(side)
+                ev_rs = torch.cuda.Event()
+                ev_rs.record(side)
+        self.bwd_local()
+        if self.has_dist:
+            main.wait_event(ev_rs)
 
     def forward_peer(self, q_src, k_src, v_src, side):
         """Eq. 2 with the a6 exchange as one peer-gather pass: pack; signal 'packed K/V ready'; on the
@@ -377,6 +439,36 @@ def loopback_peer_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
     for x in ranks:
         x.bwd_local()
     del N
+    return ranks
+
+
+def loopback_peer_fused_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
+    """Row f3 step two on ONE GPU in one process: the peer gather for the forward, and the
+    distributed backward red-adding into the other emulated ranks' owned accumulators (their
+    addresses as the 'peer' table); the ranks run in order, so no flags are needed."""
+    for r, x in enumerate(ranks):
+        x.pack_qkv(q_srcs[r], k_srcs[r], v_srcs[r])
+        x.pack_do(do_srcs[r])
+    if ranks[0].has_dist:
+        addr = lambda name: torch.tensor([getattr(y, name).data_ptr() for y in ranks], dtype=torch.int64,  # noqa: E731
+                                         device=ranks[0].dev)
+        for x in ranks:
+            x.peer_k, x.peer_v = addr("k"), addr("v")
+            x.peer_dk_acc, x.peer_dv_acc = addr("dk_acc"), addr("dv_acc")
+            x.peer_gather()
+    for x in ranks:
+        x.fwd_local()
+        if x.has_dist:
+            x.fwd_dist()
+    if ranks[0].has_dist:
+        for x in ranks:
+            x.acc_zero()
+        for x in ranks:
+            x.bwd_dist_fused()
+        for x in ranks:
+            x.acc_cast()
+    for x in ranks:
+        x.bwd_local()
     return ranks
 
 

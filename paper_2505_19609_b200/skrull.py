@@ -397,6 +397,27 @@ def skr_attn_bwd(shape, segs: DeviceSegs, q, k, v, o, dout, lse, dq, dk, dv, kv_
               ws.numel() * ws.element_size(), _stream(stream)))
 
 
+def skr_attn_bwd_peer(shape, segs: DeviceSegs, q, k, v, o, dout, lse, dq, peer_dk, peer_dv, row_map, pad_rows_P, ws,
+                      stream=None):
+    """Row f3 step two: backward of the distributed chunks with the dK / dV partials red-added into
+    the owners' fp32 accumulators (peer_dk / peer_dv: int64 device tensors of addresses)."""
+    fn = _sig("skr_attn_bwd_peer", i32, P(skr_attn_shape), P(skr_segs), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32,
+              i32, i32, vp, C.c_size_t, vp)
+    g = segs.struct()
+    _check(fn(C.byref(shape), C.byref(g), _tptr(q), _tptr(k), _tptr(v), _tptr(o), _tptr(dout), _tptr(lse), _tptr(dq),
+              _tptr(peer_dk), _tptr(peer_dv), _tptr(row_map), int(pad_rows_P), q.shape[0], k.shape[0], _tptr(ws),
+              ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def skr_pack_owner_rows(chunk_table, natural_rows):
+    """-> int32 [natural_rows]: natural row -> owner * P + row in the owner's distributed prefix."""
+    t = np.ascontiguousarray(chunk_table, np.int32).reshape(-1)
+    out = np.zeros(max(int(natural_rows), 0), np.int32)
+    _check(_sig("skr_pack_owner_rows", i32, P(i32), i32, i32, P(i32))(
+        _ptr(t, i32), len(t) // 6, int(natural_rows), _ptr(out, i32)))
+    return out
+
+
 def _rowbytes(t):
     return t[0].numel() * t.element_size() if t.shape[0] else 0
 

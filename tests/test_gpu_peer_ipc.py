@@ -2,8 +2,9 @@
 and the epoch flags, on one B200 (both ranks on cuda:0 -- IPC between processes of the same device
 is the same mechanism that maps a peer GPU's memory over NVLink). gloo carries the control plane
 (IPC blobs); the data plane is the library's peer-gather / peer-reduce / signal / wait kernels.
-Each rank runs forward_peer + backward_peer of its CP rank; the parent checks every output
-against the fp64 oracle (sharded == unsharded)."""
+Each rank runs forward_peer + backward_peer (step one: peer-reduce pass) or backward_peer_fused
+(step two: the backward kernel red-adds dK/dV into the owners' accumulators in the other process)
+of its CP rank; the parent checks every output against the fp64 oracle (sharded == unsharded)."""
 import os
 import socket
 
@@ -27,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mode):
     import torch.distributed as dist
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -51,7 +52,7 @@ def _worker(rank, world, port, q):
         side = torch.cuda.Stream()
         for _ in range(2):                      # twice: the epochs must also order buffer reuse
             rs.forward_peer(src["q"], src["k"], src["v"], side)
-            rs.backward_peer(src["do"], side)
+            (rs.backward_peer_fused if mode == "fused" else rs.backward_peer)(src["do"], side)
         torch.cuda.synchronize()
         peer.check()
         f = lambda t: t[:rs.rows].float().cpu().numpy()  # noqa: E731
@@ -68,14 +69,15 @@ def _worker(rank, world, port, q):
             dist.destroy_process_group()
 
 
-def test_peer_exchange_two_processes():
+@pytest.mark.parametrize("mode", ["step1", "fused"])
+def test_peer_exchange_two_processes(mode):
     from oracle.attention import attn_bwd, attn_fwd
     from tests.attn_harness import make_inputs, tol_ok
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
@@ -100,5 +102,5 @@ def test_peer_exchange_two_processes():
         for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
             got = outs[key][s]
             assert not np.isnan(got).any(), f"{key} seq {s}: rows not covered"
-            ok, err, bound = tol_ok(got, ref, False, label=f"{key} peer-ipc")
+            ok, err, bound = tol_ok(got, ref, False, label=f"{key} peer-ipc-{mode}")
             assert ok, f"{key} seq {s} (len {LENS[s]}): err {err} > {bound}"

@@ -167,6 +167,40 @@ def test_pack_bit_exact_fuzz():
             assert r["n_dist_seg"] == o.n_dist_seg
 
 
+def test_owner_row_map(golden):
+    # row f3 step two: natural distributed row -> owner * P + prefix row. Pinned to the hand-traced
+    # toy C1 gathered rows and, by fuzz, to the oracle packer's chunk table: each
+    # chunk's rows map to consecutive rows of its owner's prefix, and every owner prefix row of a
+    # distributed sequence is hit exactly once.
+    L, A = [17, 33, 64, 90, 128, 200, 256, 300], [-1, 1, -1, 1, 0, 1, 0, -1]
+    m = skrull.skr_pack_owner_rows(skrull.skr_pack_chunks(L, A, 2), 381)
+    P = 191
+    # 17c0 -> 0, 17c1 -> 191, 17c2 -> 195, 17c3 -> 4; 64c0 -> 9; 300c3 -> 116 (natural base 81 + 225)
+    assert list(m[0:17]) == [0, 1, 2, 3, 191, 192, 193, 194, 195, 196, 197, 198, 4, 5, 6, 7, 8]
+    assert m[17] == 9 and m[81 + 225] == 116 and m[81 + 75] == 231
+    rng = random.Random(41)
+    for _ in range(200):
+        N = rng.choice([1, 2, 3, 4, 8])
+        K = rng.randint(0, 30)
+        L = [rng.randint(0, 2000) for _ in range(K)]
+        A = [rng.randint(-1, N - 1) for _ in range(K)]
+        ref = pack_microbatch(L, A, N)
+        nat = sum(S for S, a in zip(L, A) if a == -1)
+        m = skrull.skr_pack_owner_rows(skrull.skr_pack_chunks(L, A, N), nat)
+        want = np.full(nat, -1)
+        for c in ref.chunks:
+            want[c["natural_row"]:c["natural_row"] + c["len"]] = c["gathered_row"] + np.arange(c["len"])
+        assert np.array_equal(m, want)
+        P = ref.pad_rows
+        if P:
+            owners, rows = m // P, m % P
+            for j in range(N):
+                mine = np.sort(rows[owners == j])
+                assert np.array_equal(mine, np.arange(ref.ranks[j].dist_rows))
+    with pytest.raises(skrull.SkrullError):
+        skrull.skr_pack_owner_rows(skrull.skr_pack_chunks([10], [-1], 2), 9)   # table exceeds the rows
+
+
 def test_tiles_cover_work_once_and_are_lpt_ordered():
     rng = random.Random(15)
     for _ in range(50):
