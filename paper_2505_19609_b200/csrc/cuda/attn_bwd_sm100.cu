@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const size_t row = (size_t)(kst + kvp) * a.hkv + g;
     const int which = warp / 4;
     // accumulate == 2: this key row's partial goes to its owner's accumulator (peer memory)
-    float* const peer = (accumulate == 2 && valid) ? peer_row(a, which == 0, kst + kvp) + (size_t)g * D : nullptr;
+    float* const peer = (accumulate == 2 && valid) ? peer_row(a, which == 0, kst + kvp, g, D) : nullptr;
     const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
     const float mul = which == 0 ? a.scale : 1.f;
 #pragma unroll

@@ -26,11 +26,12 @@ struct AttnArgs {
   int pad_P = 0;
 };
 
-// destination row of a dK / dV partial in accumulate mode 2 (see AttnArgs)
-__device__ __forceinline__ float* peer_row(const AttnArgs& a, bool is_dk, int krow) {
+// destination of KV head g's dK / dV partial row in accumulate mode 2 (see AttnArgs): the owner's
+// accumulator row prow, head g, d fp32 values
+__device__ __forceinline__ float* peer_row(const AttnArgs& a, bool is_dk, int krow, int g, int d) {
   const int gr = a.row_map[krow];
   const int owner = gr / a.pad_P, prow = gr - owner * a.pad_P;
-  return reinterpret_cast<float*>(is_dk ? a.peer_dk[owner] : a.peer_dv[owner]) + (size_t)prow * a.hkv;
+  return reinterpret_cast<float*>(is_dk ? a.peer_dk[owner] : a.peer_dv[owner]) + ((size_t)prow * a.hkv + g) * d;
 }
 
 skr_status simt_attn_fwd(const AttnArgs& a, int d, const float* q, const float* k, const float* v, float* o,

@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(256) bwd_dkv_kernel(AttnArgs a, const float* _
         }
       }
     }
-    float* pdk = accumulate == 2 ? peer_row(a, true, a.k_start[seg] + j) + (size_t)g * D : nullptr;
-    float* pdv = accumulate == 2 ? peer_row(a, false, a.k_start[seg] + j) + (size_t)g * D : nullptr;
+    float* pdk = accumulate == 2 ? peer_row(a, true, a.k_start[seg] + j, g, D) : nullptr;
+    float* pdv = accumulate == 2 ? peer_row(a, false, a.k_start[seg] + j, g, D) : nullptr;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (accumulate == 2) {
