@@ -60,12 +60,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, help="workload (default: C2, weak-scaled by N)")
+    ap.add_argument("--config", default=None, help="workload (default: S4n{N}, strong-scaled over the CP group)")
     ap.add_argument("--dp", type=int, default=1, help="DP degree of the DP x CP grid (CP = N / dp)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "peer1"],
                     help="CP exchange: NCCL all-gather / reduce-scatter; 'peer': row f3 step two (peer gather, "
                          "dK/dV reduced from the backward kernel's epilogue into the owners' memory); 'peer1': "
                          "row f3 step one (peer gather + peer-reduce pass)")
+    ap.add_argument("--bwd-band", type=int, default=None,
+                    help="query-band height of the backward work items (skr_tiles_bwd; default: the library's)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -337,7 +339,7 @@ def run_ours(args):
     g = torch.Generator(device="cuda")
     # the micro-batches run one after another: their working buffers come from one shared pool
     pool = BufferPool()
-    rsteps = [RankStep(shape, ml, ma, cp, cp_rank, alloc=pool.reserve) for ml, ma in mbs]
+    rsteps = [RankStep(shape, ml, ma, cp, cp_rank, alloc=pool.reserve, band_rows=args.bwd_band) for ml, ma in mbs]
     pool.materialize()
     for rs in rsteps:
         rs.rebind(pool.get)
@@ -587,7 +589,8 @@ def run_ours(args):
                        "rollbacks": int(plan["n_rollbacks"]),
                        "l2": "inputs larger than L2 (no flush)",
                        "parallelism": f"dp{dp}xcp{cp}" if dp > 1 else f"cp{cp}",
-                       "exchange": args.exchange if cp > 1 else None},
+                       "exchange": args.exchange if cp > 1 else None,
+                       "bwd_band_rows": int(sk.skr_attn_bwd_band_rows(shape) if args.bwd_band is None else args.bwd_band)},
             "roofline": {"bound": "tensor", "kernel": f"attn_{dom[0]} calls (rank 0, inside the timed loop; "
                                                       f"bwd includes its D-preprocess and dQ convert)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,

@@ -135,12 +135,21 @@ skr_status skr_pack_rank(const int64_t* mb_lens, const int32_t* assign, int32_t 
  * {seq, chunk, owner, gathered_row (owner*P + offset in owner's prefix), natural_row, len}. */
 skr_status skr_pack_chunks(const int64_t* mb_lens, const int32_t* assign, int32_t K_mb, int32_t cp,
                            int32_t* chunk_table);
-/* Attention work lists (host): pairs {segment, tile} ordered longest-work-first (LPT).
- * fwd: query tiles of block_m rows; bwd: key tiles of block_n rows over [0, k_len). */
+/* Attention work lists (host; the caller owns `tiles`, cap_tiles = its capacity in items; on
+ * SKR_E_CAPACITY *n_tiles is the number needed).
+ * fwd: pairs {segment, query tile} of block_m rows, ordered longest-work-first (LPT).
+ * bwd: quadruples {segment, key tile, q_lo, q_hi}: key tile t of block_n keys over [0, k_len) with the
+ *   segment-relative query rows [q_lo, q_hi) it processes (only those that also see the tile, i.e.
+ *   query position >= key position). band_rows = 0, or a segment of at most band_rows queries: one
+ *   item per key tile, q_lo = 0, q_hi = q_len. Longer segments are split into query bands
+ *   [b*band_rows, (b+1)*band_rows) (band_rows a multiple of 128), one item per (key tile, band) that
+ *   holds a visible query; these come first, segment by segment and band by band with key tiles
+ *   ascending (the CTAs in flight share one band's Q / dO / dQ rows in L2), then the rest in LPT
+ *   order. skr_attn_bwd sums the bands' dK / dV partials (fp32) before writing dK / dV. */
 skr_status skr_tiles_fwd(const int32_t* cu_seqlens_q, const int32_t* q_pos, int32_t n_seg, int32_t block_m,
                          int32_t* tiles, int32_t cap_tiles, int32_t* n_tiles);
 skr_status skr_tiles_bwd(const int32_t* cu_seqlens_q, const int32_t* q_pos, const int32_t* k_len, int32_t n_seg,
-                         int32_t block_n, int32_t* tiles, int32_t cap_tiles, int32_t* n_tiles);
+                         int32_t block_n, int32_t band_rows, int32_t* tiles, int32_t cap_tiles, int32_t* n_tiles);
 
 /* ------------------------------------------------------------------ a5-a9: device
  * All pointers below are DEVICE pointers; `stream` is a cudaStream_t passed as void*. */
@@ -155,7 +164,7 @@ typedef struct {                /* one segment class (locals, or distributed chu
   const int32_t* q_pos;         /* [n_seg] position of the first query in its sequence */
   const int32_t* k_start;       /* [n_seg] first row of the segment's keys in the K/V buffer */
   const int32_t* k_len;         /* [n_seg] number of keys = q_pos + q_len */
-  const int32_t* tiles;         /* [2*n_tiles] work list from skr_tiles_fwd / skr_tiles_bwd */
+  const int32_t* tiles;         /* work list: [2*n_tiles] from skr_tiles_fwd, [4*n_tiles] from skr_tiles_bwd */
   int32_t n_seg, n_tiles;
   int32_t row_begin, row_end;   /* host ints: the class's packed query rows are [row_begin, row_end) */
 } skr_segs;
@@ -172,6 +181,8 @@ typedef struct {                /* one segment class (locals, or distributed chu
  * (libskrull_fwd2sm.so, built with -DSKR_FWD_2SM_BUILD; fixed per library build, never switched at run time). */
 int32_t skr_attn_block_m(const skr_attn_shape* s);
 int32_t skr_attn_block_n(const skr_attn_shape* s);
+/* The library's query-band height for skr_tiles_bwd (0 = no bands) for this shape. */
+int32_t skr_attn_bwd_band_rows(const skr_attn_shape* s);
 skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k, const void* v,
                         void* o, float* lse, int32_t n_q_rows, int32_t n_kv_rows, void* stream);
 /* Backward (row a8): D = rowsum(dO o O); dQ, dK, dV of the plain definition.
@@ -180,7 +191,11 @@ skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* 
  *   (locals: each key row belongs to exactly one segment).
  * kv_accumulate = 1: dk, dv are fp32 [n_kv_rows][hkv][d] and are ADDED to (distributed chunks of one
  *   sequence share key rows; the caller zeroes them once).
- * ws: fp32 scratch of skr_attn_bwd_ws_bytes(). `tiles` from skr_tiles_bwd, block_n = skr_attn_block_n. */
+ * ws: fp32 scratch of skr_attn_bwd_ws_bytes(s, n_q_rows): the D rows, the fp32 dQ accumulator and
+ *   (kv_accumulate = 0 with query-banded work items) fp32 dK / dV band accumulators indexed by key row,
+ *   which is why kv_accumulate = 0 requires n_kv_rows <= n_q_rows (SKR_E_ARG otherwise; for local
+ *   segments the K / V rows are the packed query rows). `tiles` from skr_tiles_bwd with block_n =
+ *   skr_attn_block_n. */
 size_t skr_attn_bwd_ws_bytes(const skr_attn_shape* s, int32_t n_q_rows);
 skr_status skr_attn_bwd(const skr_attn_shape* s, const skr_segs* g, const void* q,
                         const void* k, const void* v, const void* o, const void* dout, const float* lse, void* dq,

@@ -1,6 +1,9 @@
 // C-ABI entry points of the attention kernels (rows a7/a8): argument checks and dispatch.
+#include <algorithm>
+
 #include "attn_common.cuh"
 #include "device.cuh"
+#include "sm100.cuh"
 
 namespace skr {
 bool fwd_two_sm();   // attn_fwd_sm100.cu: d = 128 forward on CTA pairs (the libskrull_fwd2sm.so build variant)
@@ -8,8 +11,44 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
                           int n_q_rows, int n_kv_rows, cudaStream_t st);
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
                           const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
-                          void* dv, int accumulate, float* Dbuf, float* dq_acc, int n_q_rows, int n_kv_rows,
-                          cudaStream_t st);
+                          void* dv, int accumulate, float* Dbuf, float* dq_acc, float* dk_acc, float* dv_acc,
+                          int n_q_rows, int n_kv_rows, cudaStream_t st);
+
+// Query-banded backward work items (skr_tiles_bwd): the bands of one key tile each add an fp32
+// partial dK / dV into an accumulator (ws) -- zeroed before the backward kernel and cast into dk / dv
+// after it by the item of the tile's first band. One CTA per work item: the others exit at once, the
+// owner zeroes / casts its key tile's rows for every KV head ([rows][hkv][d] is contiguous).
+__global__ void __launch_bounds__(256) band_kv_kernel(AttnArgs a, int bn, int d, int convert,
+                                                      float* __restrict__ dk_acc, float* __restrict__ dv_acc,
+                                                      void* __restrict__ dk, void* __restrict__ dv, int out_bf16) {
+  const int32_t* t = a.tiles + 4 * blockIdx.x;
+  const int seg = t[0], kv0 = t[1] * bn, q_lo = t[2], q_hi = t[3];
+  const int first_q = max(0, kv0 - a.q_pos[seg]);
+  const bool partial = q_lo > first_q || q_hi < a.cu[seg + 1] - a.cu[seg];
+  if (!partial || q_lo > first_q) return;                     // not split, or not the first band
+  const int64_t r0 = a.k_start[seg] + kv0, r1 = a.k_start[seg] + min(kv0 + bn, a.k_len[seg]);
+  const int64_t e0 = r0 * a.hkv * d / 4, e1 = r1 * a.hkv * d / 4;   // float4 index range
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    if (!convert) {
+      reinterpret_cast<float4*>(dk_acc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(dv_acc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (out_bf16) {
+      const float4 x = reinterpret_cast<const float4*>(dk_acc)[e], y = reinterpret_cast<const float4*>(dv_acc)[e];
+      reinterpret_cast<uint2*>(dk)[e] = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+      reinterpret_cast<uint2*>(dv)[e] = make_uint2(pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+    } else {
+      reinterpret_cast<float4*>(dk)[e] = reinterpret_cast<const float4*>(dk_acc)[e];
+      reinterpret_cast<float4*>(dv)[e] = reinterpret_cast<const float4*>(dv_acc)[e];
+    }
+  }
+}
+
+static skr_status band_kv(const AttnArgs& a, int bn, int d, int convert, float* dk_acc, float* dv_acc, void* dk,
+                          void* dv, int out_bf16, cudaStream_t st) {
+  if (a.n_tiles == 0) return SKR_OK;
+  band_kv_kernel<<<a.n_tiles, 256, 0, st>>>(a, bn, d, convert, dk_acc, dv_acc, dk, dv, out_bf16);
+  return launch_status(convert ? "bwd band dK/dV cast" : "bwd band dK/dV zero");
+}
 
 static skr_status check_shape(const skr_attn_shape* s) {
   if (!s) return fail(SKR_E_ARG, "null shape");
@@ -50,11 +89,25 @@ SKR_EXPORT int32_t skr_attn_block_m(const skr_attn_shape* s) {
 }
 SKR_EXPORT int32_t skr_attn_block_n(const skr_attn_shape* s) { return (s && s->dtype == SKR_FP32) ? 32 : 128; }
 
+// Query-band height of the backward work items (skr_tiles_bwd). d = 128: a band's Q / dO / dQ rows
+// for one KV group stay L2-resident while every key tile that sees them passes.
+SKR_EXPORT int32_t skr_attn_bwd_band_rows(const skr_attn_shape* s) {
+  return (s && s->dtype == SKR_BF16 && s->d == 128) ? 8192 : 0;
+}
+
+// ws layout: D [hq][n_q_rows] fp32 | bf16 only: dQ accumulator [n_q_rows][hq][d] fp32 | dK, dV band
+// accumulators [n_q_rows][hkv][d] fp32 each (indexed by key row; kv_accumulate = 0 needs
+// n_kv_rows <= n_q_rows)
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+static size_t ws_dq_off(const skr_attn_shape* s, int32_t n) { return align256((size_t)s->hq * n * 4); }
+static size_t ws_kv_off(const skr_attn_shape* s, int32_t n) {
+  return ws_dq_off(s, n) + (s->dtype == SKR_FP32 ? 0 : align256((size_t)n * s->hq * s->d * 4));
+}
+static size_t ws_kv_bytes(const skr_attn_shape* s, int32_t n) { return align256((size_t)n * s->hkv * s->d * 4); }
+
 SKR_EXPORT size_t skr_attn_bwd_ws_bytes(const skr_attn_shape* s, int32_t n_q_rows) {
   if (!s || n_q_rows < 0) return 0;
-  const size_t Dbytes = ((size_t)s->hq * n_q_rows * 4 + 255) & ~size_t(255);
-  if (s->dtype == SKR_FP32) return Dbytes;
-  return Dbytes + (size_t)n_q_rows * s->hq * s->d * 4;   // + fp32 dQ accumulator
+  return ws_kv_off(s, n_q_rows) + 2 * ws_kv_bytes(s, n_q_rows);
 }
 
 SKR_EXPORT skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
@@ -115,6 +168,8 @@ static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, cons
   const size_t need = skr_attn_bwd_ws_bytes(s, n_q_rows);
   if (ws_bytes < need) return fail(SKR_E_CAPACITY, "skr_attn_bwd: workspace %zu < %zu bytes", ws_bytes, need);
   if (skr_status e = check_sm100()) return e;
+  SKR_REQUIRE(kv_accumulate != 0 || n_kv_rows <= n_q_rows,
+              "skr_attn_bwd: kv_accumulate = 0 needs n_kv_rows (%d) <= n_q_rows (%d)", n_kv_rows, n_q_rows);
   AttnArgs a = make_args(s, g, n_q_rows);
   a.peer_dk = peer_dk;
   a.peer_dv = peer_dv;
@@ -122,15 +177,23 @@ static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, cons
   a.pad_P = pad_P;
   cudaStream_t st = (cudaStream_t)stream;
   float* Dbuf = (float*)ws;
-  if (s->dtype == SKR_FP32) {
-    if (kv_accumulate == 0) {
-      // locals: dk/dv rows are written by exactly one segment; fp32 mode writes them directly
-    }
-    return simt_attn_bwd(a, s->d, g->row_begin, g->row_end, (const float*)q, (const float*)k, (const float*)v,
-                         (const float*)o, (const float*)dout, lse, (float*)dq, (float*)dk, (float*)dv, kv_accumulate,
-                         Dbuf, st);
+  float* dk_acc = (float*)((uint8_t*)ws + ws_kv_off(s, n_q_rows));
+  float* dv_acc = (float*)((uint8_t*)dk_acc + ws_kv_bytes(s, n_q_rows));
+  const int bn = skr_attn_block_n(s), bf16 = s->dtype == SKR_BF16;
+  // kv_accumulate = 0: the key tiles split into query bands sum their partials in dk_acc / dv_acc
+  if (kv_accumulate == 0)
+    if (skr_status e = band_kv(a, bn, s->d, 0, dk_acc, dv_acc, dk, dv, bf16, st)) return e;
+  skr_status e;
+  if (!bf16) {
+    e = simt_attn_bwd(a, s->d, g->row_begin, g->row_end, (const float*)q, (const float*)k, (const float*)v,
+                      (const float*)o, (const float*)dout, lse, (float*)dq, (float*)dk, (float*)dv, kv_accumulate,
+                      Dbuf, dk_acc, dv_acc, st);
+  } else {
+    float* dq_acc = (float*)((uint8_t*)ws + ws_dq_off(s, n_q_rows));
+    e = sm100_attn_bwd(a, s->d, g->row_begin, g->row_end, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate, Dbuf,
+                       dq_acc, dk_acc, dv_acc, n_q_rows, n_kv_rows, st);
   }
-  float* dq_acc = (float*)((uint8_t*)ws + (((size_t)s->hq * n_q_rows * 4 + 255) & ~size_t(255)));
-  return sm100_attn_bwd(a, s->d, g->row_begin, g->row_end, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate, Dbuf,
-                        dq_acc, n_q_rows, n_kv_rows, st);
+  if (e) return e;
+  if (kv_accumulate == 0) return band_kv(a, bn, s->d, 1, dk_acc, dv_acc, dk, dv, bf16, st);
+  return SKR_OK;
 }

@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, AttnArgs a, const float* __restrict__ lse,
                     const float* __restrict__ Dbuf, void* __restrict__ dk_out, void* __restrict__ dv_out,
-                    int accumulate, float* __restrict__ dq_acc, int head_major) {
+                    int accumulate, float* __restrict__ dq_acc, float* __restrict__ dk_acc,
+                    float* __restrict__ dv_acc, int head_major) {
   using C = Cfg<D>;
   constexpr int BQ = C::BQ, H = C::H;
   extern __shared__ uint8_t smem_raw[];
@@ -163,13 +164,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int g = head_major ? blockIdx.y : blockIdx.x;
   const int bt = head_major ? blockIdx.x : blockIdx.y;
-  const int seg = a.tiles[2 * bt], ktile = a.tiles[2 * bt + 1];
+  // work item {seg, key tile, q_lo, q_hi} (skr_tiles_bwd): the key tile against the segment-relative
+  // queries [q_lo, q_hi) that see it; a band of a split tile (partial) adds its dK / dV in fp32
+  const int32_t* item = a.tiles + 4 * bt;
+  const int seg = item[0], ktile = item[1], q_lo = item[2], q_hi = item[3];
   const int grp = a.hq / a.hkv;
   const int cu0 = a.cu[seg], q_len = a.cu[seg + 1] - cu0;
   const int q_pos = a.q_pos[seg], k_len = a.k_len[seg], kst = a.k_start[seg];
   const int kv0 = ktile * BN;
-  const int i_first = max(0, kv0 - q_pos);          // first query (segment-relative) that sees the tile
-  const int qt_first = i_first / BQ, qt_last = (q_len - 1) / BQ;
+  const int i_vis = max(0, kv0 - q_pos);            // first query (segment-relative) that sees the tile
+  const bool partial = q_lo > i_vis || q_hi < q_len;
+  const int i_first = max(i_vis, q_lo);             // band edges are multiples of 128, so of BQ
+  const int qt_first = i_first / BQ, qt_last = (min(q_len, q_hi) - 1) / BQ;
   const int n_steps = grp * (qt_last - qt_first + 1);
 
   if (threadIdx.x == 0) {
@@ -599,8 +605,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool valid = kvp < k_len;
     const size_t row = (size_t)(kst + kvp) * a.hkv + g;
     const int which = warp / 4;
-    // accumulate == 2: this key row's partial goes to its owner's accumulator (peer memory)
+    // accumulate == 2: this key row's partial goes to its owner's accumulator (peer memory);
+    // accumulate == 0 and a band of a split tile: into the band accumulator (cast after the launch)
     float* const peer = (accumulate == 2 && valid) ? peer_row(a, which == 0, kst + kvp, g, D) : nullptr;
+    float* const acc_f32 = accumulate == 2   ? peer
+                           : accumulate == 1 ? reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D
+                           : partial         ? (which == 0 ? dk_acc : dv_acc) + row * D
+                                             : nullptr;
     const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
     const float mul = which == 0 ? a.scale : 1.f;
 #pragma unroll
@@ -609,8 +620,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32(tmem + lane_base + tcol + c, r);
       tmem_wait_ld();
       if (!valid) continue;
-      if (accumulate) {
-        float* dst = accumulate == 2 ? peer + c : reinterpret_cast<float*>(which == 0 ? dk_out : dv_out) + row * D + c;
+      if (acc_f32 != nullptr) {
+        float* dst = acc_f32 + c;
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
           red_add_v4(dst + i, __uint_as_float(r[i]) * mul, __uint_as_float(r[i + 1]) * mul,
@@ -821,8 +832,8 @@ extern "C" __attribute__((visibility("default"))) int skr_debug_bwd_trace(unsign
 
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
                           const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
-                          void* dv, int accumulate, float* Dbuf, float* dq_acc, int n_q_rows, int n_kv_rows,
-                          cudaStream_t st) {
+                          void* dv, int accumulate, float* Dbuf, float* dq_acc, float* dk_acc, float* dv_acc,
+                          int n_q_rows, int n_kv_rows, cudaStream_t st) {
   trace_buffer();
   if (d != 64 && d != 128) return fail(SKR_E_UNSUPPORTED, "bf16 backward supports d in {64,128}");
   const int rows = row_end - row_begin;
@@ -864,7 +875,7 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
     auto launch = [&](auto kern, int smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       kern<<<grid, bwd::kThreads, smem, st>>>(tq, tk, tv, tdo, tdq, a, lse, Dbuf, dk, dv, accumulate, dq_acc,
-                                              head_major);
+                                              dk_acc, dv_acc, head_major);
     };
     if (d == 128) {
       constexpr int smem = bwd::Cfg<128>::kSmem;

@@ -12,7 +12,7 @@ struct AttnArgs {
   const int32_t* q_pos;    // [n_seg]
   const int32_t* k_start;  // [n_seg]
   const int32_t* k_len;    // [n_seg]
-  const int32_t* tiles;    // [2*n_tiles] {seg, tile}
+  const int32_t* tiles;    // fwd [2*n_tiles] {seg, tile}; bwd [4*n_tiles] {seg, key tile, q_lo, q_hi}
   int n_seg, n_tiles;
   int hq, hkv;
   float scale;
@@ -38,6 +38,6 @@ skr_status simt_attn_fwd(const AttnArgs& a, int d, const float* q, const float* 
                          float* lse, cudaStream_t st);
 skr_status simt_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const float* q, const float* k,
                          const float* v, const float* o, const float* dout, const float* lse, float* dq, float* dk,
-                         float* dv, int accumulate, float* Dbuf, cudaStream_t st);
+                         float* dv, int accumulate, float* Dbuf, float* dk_acc, float* dv_acc, cudaStream_t st);
 
 }  // namespace skr

@@ -603,7 +603,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
       PhaseAcct pa;   // 0 wait S, 1 TMEM load S, 2 mask + max + exchange, 3 wait PV, 4 rescale + store P, 6 exps
       pa.start();
       for (int j = 0; j < n_kv; ++j) {
-        mbar_wait(&bars->s_full[s], j & 1);
+        mbar_wait(&bars->s_full[s], j & 1);   // (a suspend-hinted wait measured the same, r02_run12)
         pa.mark(0);
         tc_fence_after();
         float x[HN];

@@ -166,14 +166,21 @@ __global__ void __launch_bounds__(256) bwd_dkv_kernel(AttnArgs a, const float* _
                                                       const float* __restrict__ k, const float* __restrict__ v,
                                                       const float* __restrict__ dout, const float* __restrict__ lse,
                                                       const float* __restrict__ Dbuf, float* __restrict__ dk,
-                                                      float* __restrict__ dv, int accumulate) {
+                                                      float* __restrict__ dv, int accumulate,
+                                                      float* __restrict__ dk_acc, float* __restrict__ dv_acc) {
   constexpr int E = D / 32;
-  const int seg = a.tiles[2 * blockIdx.x], tile = a.tiles[2 * blockIdx.x + 1];
+  // work item {seg, key tile, q_lo, q_hi} (skr_tiles_bwd): queries [q_lo, q_hi) of the segment
+  const int32_t* item = a.tiles + 4 * blockIdx.x;
+  const int seg = item[0], tile = item[1], q_lo = item[2], q_hi = item[3];
   const int g = blockIdx.y, grp = a.hq / a.hkv;
   const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
   const int qpos = a.q_pos[seg], qlen = cu1 - cu0, klen = a.k_len[seg];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int per_warp = kBN / kWarps;
+  // a band of a split key tile: its partial is added into the band accumulator (locals) or the
+  // caller's fp32 accumulator (kv_accumulate 1 / 2)
+  const bool partial = q_lo > max(0, tile * kBN - qpos) || q_hi < qlen;
+  const int q_end = min(qlen, q_hi);
   for (int i = 0; i < per_warp; ++i) {
     const int j = tile * kBN + warp * per_warp + i;  // key position
     if (j >= klen) break;
@@ -185,10 +192,10 @@ __global__ void __launch_bounds__(256) bwd_dkv_kernel(AttnArgs a, const float* _
       vr[e] = v[ko + lane + 32 * e];
       ak[e] = av[e] = 0.f;
     }
-    const int i0 = max(0, j - qpos);  // first query (segment-relative) that sees key j
+    const int i0 = max(max(0, j - qpos), q_lo);  // first query (segment-relative) of the item that sees key j
     for (int hh = 0; hh < grp; ++hh) {
       const int h = g * grp + hh;
-      for (int r = i0; r < qlen; ++r) {
+      for (int r = i0; r < q_end; ++r) {
         const size_t qo = ((size_t)(cu0 + r) * a.hq + h) * D;
         float s = 0.f, dp = 0.f;
 #pragma unroll
@@ -217,6 +224,9 @@ __global__ void __launch_bounds__(256) bwd_dkv_kernel(AttnArgs a, const float* _
       } else if (accumulate) {
         atomicAdd(&dk[ko + lane + 32 * e], ak[e] * a.scale);
         atomicAdd(&dv[ko + lane + 32 * e], av[e]);
+      } else if (partial) {
+        atomicAdd(&dk_acc[ko + lane + 32 * e], ak[e] * a.scale);
+        atomicAdd(&dv_acc[ko + lane + 32 * e], av[e]);
       } else {
         dk[ko + lane + 32 * e] = ak[e] * a.scale;
         dv[ko + lane + 32 * e] = av[e];
@@ -244,7 +254,7 @@ skr_status simt_attn_fwd(const AttnArgs& a, int d, const float* q, const float* 
 
 skr_status simt_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const float* q, const float* k,
                          const float* v, const float* o, const float* dout, const float* lse, float* dq, float* dk,
-                         float* dv, int accumulate, float* Dbuf, cudaStream_t st) {
+                         float* dv, int accumulate, float* Dbuf, float* dk_acc, float* dv_acc, cudaStream_t st) {
   if (row_end > row_begin) {
     const int warps = (row_end - row_begin) * a.hq;
     const int blocks = (warps * 32 + 255) / 256;
@@ -264,11 +274,11 @@ skr_status simt_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, c
   if (a.n_tiles) {
     dim3 grid(a.n_tiles, a.hkv);
     if (d == 64)
-      simt::bwd_dkv_kernel<64><<<grid, 256, 0, st>>>(a, q, k, v, dout, lse, Dbuf, dk, dv, accumulate);
+      simt::bwd_dkv_kernel<64><<<grid, 256, 0, st>>>(a, q, k, v, dout, lse, Dbuf, dk, dv, accumulate, dk_acc, dv_acc);
     else if (d == 128)
-      simt::bwd_dkv_kernel<128><<<grid, 256, 0, st>>>(a, q, k, v, dout, lse, Dbuf, dk, dv, accumulate);
+      simt::bwd_dkv_kernel<128><<<grid, 256, 0, st>>>(a, q, k, v, dout, lse, Dbuf, dk, dv, accumulate, dk_acc, dv_acc);
     else
-      simt::bwd_dkv_kernel<32><<<grid, 256, 0, st>>>(a, q, k, v, dout, lse, Dbuf, dk, dv, accumulate);
+      simt::bwd_dkv_kernel<32><<<grid, 256, 0, st>>>(a, q, k, v, dout, lse, Dbuf, dk, dv, accumulate, dk_acc, dv_acc);
   }
   return launch_status("simt bwd");
 }

@@ -214,20 +214,49 @@ SKR_EXPORT skr_status skr_tiles_fwd(const int32_t* cu, const int32_t* q_pos, int
 }
 
 SKR_EXPORT skr_status skr_tiles_bwd(const int32_t* cu, const int32_t* q_pos, const int32_t* k_len, int32_t n_seg,
-                                    int32_t bn, int32_t* tiles, int32_t cap, int32_t* n_tiles) {
+                                    int32_t bn, int32_t band_rows, int32_t* tiles, int32_t cap, int32_t* n_tiles) {
   SKR_REQUIRE(n_tiles && bn > 0 && n_seg >= 0 && (n_seg == 0 || (cu && q_pos && k_len)) && (cap == 0 || tiles),
               "skr_tiles_bwd: bad arguments");
-  std::vector<Tile> v;
+  SKR_REQUIRE(band_rows >= 0 && band_rows % 128 == 0, "skr_tiles_bwd: band_rows %d must be a multiple of 128",
+              band_rows);
+  // Segments longer than band_rows are split into query bands [b * band_rows, (b + 1) * band_rows):
+  // one work item per (key tile, band), ordered segment by segment, band by band, key tiles
+  // ascending, so the CTAs in flight share one band's Q / dO / dQ rows (L2-resident) instead of each
+  // streaming its key tile's whole query range. The rest: one item per key tile, LPT-ordered, after
+  // the banded items (they also form the tail of the launch).
+  struct Item {
+    int32_t seg, tile, q_lo, q_hi;
+    int64_t work;
+  };
+  std::vector<Item> banded, whole;
   for (int32_t s = 0; s < n_seg; ++s) {
     const int64_t ql = cu[s + 1] - cu[s];
+    SKR_REQUIRE(ql >= 0, "skr_tiles_bwd: cu_seqlens not monotone at %d", s);
     if (ql <= 0) continue;
-    const int64_t q_end = (int64_t)q_pos[s] + ql;
-    for (int64_t t = 0; t * bn < k_len[s]; ++t) {
-      const int64_t first_q = std::max<int64_t>(q_pos[s], t * bn);   // queries that see this key tile
-      v.push_back({s, (int32_t)t, q_end - first_q});
+    const bool split = band_rows > 0 && ql > band_rows;
+    const int64_t nb = split ? (ql + band_rows - 1) / band_rows : 1;
+    for (int64_t b = 0; b < nb; ++b) {
+      for (int64_t t = 0; t * bn < k_len[s]; ++t) {
+        // queries (segment-relative) that see this key tile: [first_q, ql)
+        const int64_t first_q = std::max<int64_t>(q_pos[s], t * bn) - q_pos[s];
+        const int64_t lo = split ? b * band_rows : 0, hi = split ? std::min<int64_t>(ql, (b + 1) * band_rows) : ql;
+        if (std::max(lo, first_q) >= hi) continue;
+        (split ? banded : whole).push_back({s, (int32_t)t, (int32_t)lo, (int32_t)hi, hi - std::max(lo, first_q)});
+      }
     }
   }
-  return emit_tiles(v, tiles, cap, n_tiles);
+  // LPT for the whole-range items: heaviest first; ties by (segment, tile) for determinism
+  std::sort(whole.begin(), whole.end(), [](const Item& a, const Item& b) {
+    if (a.work != b.work) return a.work > b.work;
+    if (a.seg != b.seg) return a.seg < b.seg;
+    return a.tile < b.tile;
+  });
+  *n_tiles = (int32_t)(banded.size() + whole.size());
+  if ((int64_t)*n_tiles > cap) return skr::fail(SKR_E_CAPACITY, "tiles: need %d entries", *n_tiles);
+  int32_t* o = tiles;
+  for (const auto* v : {&banded, &whole})
+    for (const Item& x : *v) o[0] = x.seg, o[1] = x.tile, o[2] = x.q_lo, o[3] = x.q_hi, o += 4;
+  return SKR_OK;
 }
 
 SKR_EXPORT skr_status skr_pack_owner_rows(const int32_t* table, int32_t n_chunks, int32_t natural_rows,

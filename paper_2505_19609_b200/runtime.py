@@ -63,9 +63,10 @@ def _alloc_new(device):
 
 
 class RankStep:
-    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda", alloc=None):
+    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda", alloc=None, band_rows=None):
         """alloc(name, shape, dtype) -> tensor: where the working buffers come from (default: fresh
-        allocations; BufferPool.reserve to share them across micro-batches)."""
+        allocations; BufferPool.reserve to share them across micro-batches). band_rows: query-band
+        height of the backward work lists (skr_tiles_bwd; None = the library's choice)."""
         self.shape, self.cp, self.rank = shape, cp, rank
         self.dev = device
         self._alloc = alloc or _alloc_new(device)
@@ -87,9 +88,9 @@ class RankStep:
         self.src_row = torch.as_tensor(pr["src_row"]).to(device)
         # segment classes: distributed chunks [0, nd), locals [nd, ns)
         self.dist_f = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "fwd", device)
-        self.dist_b = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "bwd", device)
+        self.dist_b = sk.make_segs(shape, cu[:nd + 1], qp[:nd], ks[:nd], kl[:nd], "bwd", device, band_rows)
         self.loc_f = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "fwd", device)
-        self.loc_b = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "bwd", device)
+        self.loc_b = sk.make_segs(shape, cu[nd:], qp[nd:], ks[nd:], kl[nd:], "bwd", device, band_rows)
         if self.has_dist:
             table = sk.skr_pack_chunks(mb_lens, assign, cp)
             self.chunks = torch.as_tensor(table.reshape(-1)).to(device)
@@ -164,7 +165,8 @@ class RankStep:
         if self.rows:
             n += 4                                            # pack Q, K, V, dO
         loc_rows = self.loc_b.row_end - self.loc_b.row_begin
-        n += (self.loc_f.n_tiles > 0) + (self.loc_b.n_tiles > 0) + 2 * (loc_rows > 0)
+        # local bwd: + the band accumulator zero / cast launches (kv_accumulate = 0)
+        n += (self.loc_f.n_tiles > 0) + 3 * (self.loc_b.n_tiles > 0) + 2 * (loc_rows > 0)
         if self.has_dist:
             dist_rows = self.dist_b.row_end - self.dist_b.row_begin
             n += (self.dist_f.n_tiles > 0) + (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)

@@ -303,23 +303,24 @@ def skr_pack_chunks(mb_lens, assign, cp):
     return t
 
 
-def _tiles(fn_name, cu, q_pos, k_len, n_seg, block):
+def _tiles(fn_name, cu, q_pos, k_len, n_seg, block, band_rows=0):
     cu = np.ascontiguousarray(cu, np.int32)
     qp = np.ascontiguousarray(q_pos, np.int32)
+    width = 2 if fn_name == "skr_tiles_fwd" else 4     # {seg, tile} / {seg, key tile, q_lo, q_hi}
     n = i32()
     cap = 0
     for _ in range(2):
-        out = np.zeros(2 * max(cap, 1), np.int32)
+        out = np.zeros(width * max(cap, 1), np.int32)
         if fn_name == "skr_tiles_fwd":
             st = _sig(fn_name, i32, P(i32), P(i32), i32, i32, P(i32), i32, P(i32))(
                 _ptr(cu, i32), _ptr(qp, i32), int(n_seg), int(block), _ptr(out, i32), cap, C.byref(n))
         else:
             kl = np.ascontiguousarray(k_len, np.int32)
-            st = _sig(fn_name, i32, P(i32), P(i32), P(i32), i32, i32, P(i32), i32, P(i32))(
-                _ptr(cu, i32), _ptr(qp, i32), _ptr(kl, i32), int(n_seg), int(block), _ptr(out, i32), cap,
-                C.byref(n))
+            st = _sig(fn_name, i32, P(i32), P(i32), P(i32), i32, i32, i32, P(i32), i32, P(i32))(
+                _ptr(cu, i32), _ptr(qp, i32), _ptr(kl, i32), int(n_seg), int(block), int(band_rows), _ptr(out, i32),
+                cap, C.byref(n))
         if st == SKR_OK:
-            return out[:2 * n.value].reshape(-1, 2)
+            return out[:width * n.value].reshape(-1, width)
         if st != SKR_E_CAPACITY:
             _check(st)
         cap = n.value
@@ -330,8 +331,8 @@ def skr_tiles_fwd(cu, q_pos, n_seg, block_m):
     return _tiles("skr_tiles_fwd", cu, q_pos, None, n_seg, block_m)
 
 
-def skr_tiles_bwd(cu, q_pos, k_len, n_seg, block_n):
-    return _tiles("skr_tiles_bwd", cu, q_pos, k_len, n_seg, block_n)
+def skr_tiles_bwd(cu, q_pos, k_len, n_seg, block_n, band_rows=0):
+    return _tiles("skr_tiles_bwd", cu, q_pos, k_len, n_seg, block_n, band_rows)
 
 
 # ---------------------------------------------------------------------------- a5-a9 device
@@ -347,6 +348,10 @@ def skr_attn_block_n(shape) -> int:
     return _sig("skr_attn_block_n", i32, P(skr_attn_shape))(C.byref(shape))
 
 
+def skr_attn_bwd_band_rows(shape) -> int:
+    return _sig("skr_attn_bwd_band_rows", i32, P(skr_attn_shape))(C.byref(shape))
+
+
 def skr_attn_bwd_ws_bytes(shape, n_q_rows) -> int:
     return _sig("skr_attn_bwd_ws_bytes", C.c_size_t, P(skr_attn_shape), i32)(C.byref(shape), int(n_q_rows))
 
@@ -360,8 +365,9 @@ class DeviceSegs:
         self.n_seg = len(cu) - 1
         t = lambda x: torch.as_tensor(np.ascontiguousarray(x, np.int32)).to(device)  # noqa: E731
         self.cu, self.q_pos, self.k_start, self.k_len = t(cu), t(q_pos), t(k_start), t(k_len)
-        self.tiles = t(np.asarray(tiles, np.int32).reshape(-1))
-        self.n_tiles = len(self.tiles) // 2
+        tiles = np.asarray(tiles, np.int32)
+        self.tiles = t(tiles.reshape(-1))
+        self.n_tiles = tiles.shape[0] if tiles.ndim == 2 else 0
         self.row_begin = int(cu[0]) if row_begin is None else int(row_begin)
         self.row_end = int(cu[-1]) if row_end is None else int(row_end)
 
@@ -371,13 +377,15 @@ class DeviceSegs:
                         self.row_end)
 
 
-def make_segs(shape, cu, q_pos, k_start, k_len, kind="fwd", device="cuda"):
-    """Host work list (skr_tiles_fwd / skr_tiles_bwd) + device tables for one segment class."""
+def make_segs(shape, cu, q_pos, k_start, k_len, kind="fwd", device="cuda", band_rows=None):
+    """Host work list (skr_tiles_fwd / skr_tiles_bwd) + device tables for one segment class.
+    band_rows (bwd): query-band height of the work items; None = the library's choice for the shape."""
     n = len(cu) - 1
     if kind == "fwd":
         tiles = skr_tiles_fwd(cu, q_pos, n, skr_attn_block_m(shape))
     else:
-        tiles = skr_tiles_bwd(cu, q_pos, k_len, n, skr_attn_block_n(shape))
+        band = skr_attn_bwd_band_rows(shape) if band_rows is None else int(band_rows)
+        tiles = skr_tiles_bwd(cu, q_pos, k_len, n, skr_attn_block_n(shape), band)
     return DeviceSegs(cu, q_pos, k_start, k_len, tiles, device=device)
 
 

@@ -102,10 +102,11 @@ def test_fwd_fp32_local():
 # ----------------------------------------------------------------------------- backward
 
 
-def _run_bwd(sk, shape, pk, kv_accumulate=False):
-    """fwd + bwd of one segment class; returns O, LSE, dQ, dK, dV (float numpy)."""
+def _run_bwd(sk, shape, pk, kv_accumulate=False, band_rows=None):
+    """fwd + bwd of one segment class; returns O, LSE, dQ, dK, dV (float numpy). band_rows: query-band
+    height of the backward work items (None: the library's choice)."""
     segs_f = sk.make_segs(shape, pk.cu, pk.q_pos, pk.k_start, pk.k_len, "fwd")
-    segs_b = sk.make_segs(shape, pk.cu, pk.q_pos, pk.k_start, pk.k_len, "bwd")
+    segs_b = sk.make_segs(shape, pk.cu, pk.q_pos, pk.k_start, pk.k_len, "bwd", band_rows=band_rows)
     o = torch.zeros_like(pk.q)
     lse = torch.zeros(shape.hq, max(pk.rows, 1), device="cuda", dtype=torch.float32)
     sk.skr_attn_fwd(shape, segs_f, pk.q, pk.k, pk.v, o, lse)
@@ -177,6 +178,31 @@ def test_bwd_bf16_peaky_softmax(hq, hkv, d):
         r += n
 
 
+@pytest.mark.parametrize("hq,hkv,d", SHAPES)
+@pytest.mark.parametrize("band", [128, 384])
+def test_bwd_bf16_query_bands(hq, hkv, d, band):
+    # key tiles split into query bands (skr_tiles_bwd band_rows): each band adds an fp32 dK / dV
+    # partial into the band accumulator, cast once after the kernel; ragged last bands, bands that
+    # start inside a key tile's diagonal, segments shorter than a band (whole items) in one launch
+    sk = _sk()
+    lens = [1, 17, 128, 129, 300, 777, 0, 256, 1100]
+    inputs = make_inputs(lens, hq, hkv, d, seed=25)
+    pk = local_pack(inputs, torch.bfloat16)
+    shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16)
+    O, L, dQ, dK, dV = _run_bwd(sk, shape, pk, band_rows=band)
+    _check_bwd_local(pk, dQ, dK, dV, fp32=False)
+
+
+def test_bwd_fp32_query_bands():
+    sk = _sk()
+    lens = [1, 33, 64, 90, 200, 300]
+    inputs = make_inputs(lens, 2, 1, 64, seed=26, bf16=False)
+    pk = local_pack(inputs, torch.float32)
+    shape = sk.attn_shape(2, 1, 64, sk.SKR_FP32)
+    O, L, dQ, dK, dV = _run_bwd(sk, shape, pk, band_rows=128)
+    _check_bwd_local(pk, dQ, dK, dV, fp32=True)
+
+
 def test_bwd_fp32_local():
     sk = _sk()
     lens = [1, 33, 64, 90, 200, 300]
@@ -188,9 +214,10 @@ def test_bwd_fp32_local():
     _check_bwd_local(pk, dQ, dK, dV, fp32=True)
 
 
+@pytest.mark.parametrize("band", [None, 256])
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
 @pytest.mark.parametrize("N", [1, 2, 3])
-def test_bwd_distributed_chunks_sum_to_unsharded(dtype, N):
+def test_bwd_distributed_chunks_sum_to_unsharded(dtype, N, band):
     # every rank's zigzag chunks (R20) against the natural K/V buffer; per-rank fp32 dK/dV
     # partials summed over ranks (the reduce-scatter's job) equal the unsharded gradients.
     sk = _sk()
@@ -213,7 +240,7 @@ def test_bwd_distributed_chunks_sum_to_unsharded(dtype, N):
             for c in (j, 2 * N - 1 - j):
                 segs.append((s, c * S // (2 * N), (c + 1) * S // (2 * N)))
         pk = Packed(inputs, segs, base, list(range(len(lens))), tdt)
-        O, L, dQ, dK, dV = _run_bwd(sk, shape, pk, kv_accumulate=True)
+        O, L, dQ, dK, dV = _run_bwd(sk, shape, pk, kv_accumulate=True, band_rows=band)
         _check_fwd(pk, O, L, fp32=not bf)
         r = 0
         for s, lo, hi in segs:

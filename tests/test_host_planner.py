@@ -214,8 +214,46 @@ def test_tiles_cover_work_once_and_are_lpt_ordered():
         w = [qp[s] + min(ql[s], (t + 1) * 128) for s, t in tf]
         assert w == sorted(w, reverse=True)
         tb = skrull.skr_tiles_bwd(cu, qp, kl, n, 128)
-        assert sorted(map(tuple, tb)) == sorted((s, t) for s in range(n) if ql[s] > 0
+        assert sorted(map(tuple, tb)) == sorted((s, t, 0, ql[s]) for s in range(n) if ql[s] > 0
                                                 for t in range(-(-kl[s] // 128)))
+        w = [ql[s] - max(0, t * 128 - qp[s]) for s, t, _, _ in tb]
+        assert w == sorted(w, reverse=True)
+
+
+def test_tiles_bwd_query_bands_cover_every_causal_pair_once():
+    # skr_tiles_bwd with band_rows: every (segment, key tile, visible query) exactly once; segments of
+    # more than band_rows queries come first, split into bands [b*B, (b+1)*B) in (segment, band, key
+    # tile) order, the rest whole and LPT-ordered after them
+    rng = random.Random(17)
+    for it in range(60):
+        n = rng.randint(0, 8)
+        ql = [rng.choice([0, 1, 127, 128, 129, 300, 700, 1024, 1500, 2500]) for _ in range(n)]
+        qp = [rng.choice([0, 0, 5, 128, 333]) for _ in range(n)]
+        cu = np.concatenate([[0], np.cumsum(ql)]).astype(np.int32)
+        kl = [a + b for a, b in zip(qp, ql)]
+        B = rng.choice([128, 256, 512, 1024])
+        bn = rng.choice([32, 128])
+        tb = skrull.skr_tiles_bwd(cu, qp, kl, n, bn, B)
+        seen = {}
+        for s, t, lo, hi in tb:
+            first = max(0, t * bn - qp[s])
+            assert 0 <= lo < hi <= ql[s] and max(lo, first) < hi
+            for i in range(max(lo, first), hi):
+                key = (s, t, i)
+                assert key not in seen
+                seen[key] = 1
+        want = {(s, t, i) for s in range(n) for t in range(-(-kl[s] // bn))
+                for i in range(max(0, t * bn - qp[s]), ql[s])}
+        assert set(seen) == want
+        split = [ql[s] > B for s, _, _, _ in tb]
+        assert split == sorted(split, reverse=True)          # banded items first
+        nb = sum(split)
+        order = [(s, lo, t) for s, t, lo, _ in tb[:nb]]
+        assert order == sorted(order)
+        assert all(lo % B == 0 and (hi == ql[s] or hi - lo == B) for s, _, lo, hi in tb[:nb])
+        assert all(lo == 0 and hi == ql[s] for s, _, lo, hi in tb[nb:])
+    with pytest.raises(skrull.SkrullError):
+        skrull.skr_tiles_bwd(np.array([0, 10], np.int32), [0], [10], 1, 128, 100)   # not a multiple of 128
 
 
 def test_baselines_bit_exact_fuzz():
