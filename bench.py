@@ -129,7 +129,7 @@ def rank_pairs(mb_lens, assign, cp, rank):
 class ClockSampler:
     FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap"
+             "clocks_event_reasons.sw_power_cap,power.limit"
 
     def __init__(self, index):
         self.index = index
@@ -166,8 +166,19 @@ class ClockSampler:
             for nm, v in zip(names, r[4:8]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
+        def num(i):
+            v = []
+            for r in self.rows:
+                try:
+                    v.append(float(r[i]))
+                except (IndexError, ValueError):
+                    pass
+            return v
+        pw, pl = num(2), num(8)
+        # clocks and power limit beside the numbers
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": float(np.median(pw)) if pw else None, "power_limit_w": max(pl) if pl else None}
 
 
 def measured_peaks():

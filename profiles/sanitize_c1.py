@@ -1,7 +1,7 @@
 """compute-sanitizer target: toy C1 (BASELINE configs[0]) at CP = 2 through the CP
 runtime with the loopback exchange, in bf16 (tcgen05 kernels) and in fp32 test mode, plus the
 composite skr_cp_attn_fwd / _bwd step on a 1-rank NCCL communicator with hand-distributed
-sequences. Small on purpose: every launch runs under the sanitizer's instrumentation.
+sequences, and the query-banded backward work lists (band_rows = 128). Small on purpose: every launch runs under the sanitizer's instrumentation.
 
     compute-sanitizer --tool memcheck python profiles/sanitize_c1.py
 """
@@ -19,12 +19,12 @@ from synth import seq_tensors  # noqa: E402
 LENS = [17, 33, 64, 90, 128, 200, 256, 300]
 
 
-def run(dtype, hq, hkv, d, N=2, C=600):
+def run(dtype, hq, hkv, d, N=2, C=600, band=None):
     shape = sk.attn_shape(hq, hkv, d, dtype)
     p = sk.skr_plan(LENS, C, N, 1, hq * d, hkv * d)
     tdt = torch.bfloat16 if dtype == sk.SKR_BF16 else torch.float32
     inputs = [seq_tensors(0, i, S, hq, hkv, d, bf16=dtype == sk.SKR_BF16) for i, S in enumerate(LENS)]
-    ranks = [RankStep(shape, np.asarray(LENS), p["assign"], N, r) for r in range(N)]
+    ranks = [RankStep(shape, np.asarray(LENS), p["assign"], N, r, band_rows=band) for r in range(N)]
     srcs = {k: [torch.from_numpy(gather_rank_natural(inputs, LENS, p["assign"], N, r, k)).to("cuda", tdt)
                 for r in range(N)] for k in ("q", "k", "v", "do")}
     loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
@@ -52,5 +52,7 @@ if __name__ == "__main__":
     run(sk.SKR_BF16, 2, 1, 64)
     run(sk.SKR_BF16, 4, 2, 128)
     run(sk.SKR_FP32, 2, 2, 64)
+    run(sk.SKR_BF16, 4, 2, 128, band=128)   # query-banded backward items (band accumulators, zero / cast)
+    run(sk.SKR_FP32, 2, 2, 64, band=128)
     run_nccl()
     print("sanitize target done")
