@@ -480,10 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int st = n % C::kStages;
       const int qp_base = q_pos + it.qt * BQ + col0;        // position of this warpgroup's first query
       const bool diag = kv0 + BN - 1 > qp_base;             // warp-uniform: causal mask needed
-      wg_mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1, 2 + wg);
+      mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1);
       if (threadIdx.x == 0) trace(14);
       const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (C::kStages * BQ + st * BQ + col0) * 4;
-      wg_mbar_wait(&bars->s_full, n & 1, 2 + wg);
+      mbar_wait(&bars->s_full, n & 1);
       pa.mark(0);
       if (threadIdx.x == 0) trace(10);
       tc_fence_after();
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kvp > qp_base + i) p[i] = 0.f;               // causal (invalid queries: lse2 = +inf -> 0)
       }
       pa.mark(2);
-      if (n > 0) wg_mbar_wait(&bars->dv_done, (n - 1) & 1, 2 + wg);     // P^T TMEM columns free
+      if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T TMEM columns free
       pa.mark(3);
       tc_fence_after();
       {
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars->p_full);
       if (threadIdx.x == 0) trace(11);
       pa.mark(4);
-      wg_mbar_wait(&bars->dp_full, n & 1, 2 + wg);
+      mbar_wait(&bars->dp_full, n & 1);
       if (threadIdx.x == 0) trace(12);
       pa.mark(5);
       tc_fence_after();
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       pa.mark(6);
-      if (n > 0) wg_mbar_wait(&bars->dsq_done, (n - 1) & 1, 2 + wg);    // dS^T smem / TMEM free
+      if (n > 0) mbar_wait(&bars->dsq_done, (n - 1) & 1);    // dS^T smem / TMEM free
       tc_fence_after();
       {
         uint32_t pk[H / 2];

@@ -603,7 +603,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
       PhaseAcct pa;   // 0 wait S, 1 TMEM load S, 2 mask + max + exchange, 3 wait PV, 4 rescale + store P, 6 exps
       pa.start();
       for (int j = 0; j < n_kv; ++j) {
-        wg_mbar_wait(&bars->s_full[s], j & 1, 3 + warp / 4);   // (a suspend-hinted wait measured the same, r02_run12)
+        mbar_wait(&bars->s_full[s], j & 1);   // (a suspend-hinted wait measured the same, r02_run12)
         pa.mark(0);
         tc_fence_after();
         float x[HN];
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         pa.mark(6);
         // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
         if (j > 0) {
-          wg_mbar_wait(&bars->pv_done[s], (j - 1) & 1, 3 + warp / 4);
+          mbar_wait(&bars->pv_done[s], (j - 1) & 1);
           tc_fence_after();
         }
         pa.mark(3);

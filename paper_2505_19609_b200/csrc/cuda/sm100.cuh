@@ -425,20 +425,6 @@ __device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Wait for an mbarrier phase by a whole warpgroup (4 consecutive warps starting at a multiple of 4).
-// SKR_ONE_POLLER builds: only the warpgroup's first warp polls the mbarrier (each poll is a shared-
-// memory access that competes with the MMA operand reads and costs energy under the power cap); the
-// other three wait in the hardware named barrier `bar_id`, which orders the poller's acquire before
-// their subsequent tcgen05.fence::after_thread_sync / loads.
-__device__ __forceinline__ void wg_mbar_wait(uint64_t* bar, uint32_t parity, int bar_id) {
-#ifdef SKR_ONE_POLLER
-  if ((threadIdx.x / 32) % 4 == 0) mbar_wait(bar, parity);
-  named_bar_sync(bar_id, 128);
-#else
-  (void)bar_id;
-  mbar_wait(bar, parity);
-#endif
-}
 
 // Phase accounting (SKR_PHASE_ACCT builds): per-warp cycle totals of each phase of the loop kept in
 // registers and written once at the end (the kernel passes its traced block's buffer) - no events on the path, so the
