@@ -57,6 +57,12 @@ constexpr int BN = 128;  // key tile
 // group's Q / dO / dQ rows. d = 128 uses 1 (S4n1 bwd DRAM 166 -> 120 GB per launch, C5n1 bwd
 // -5 %); d = 64 keeps 0 (profiles/r02_experiments.md).
 constexpr int kThreads = 448;
+// scale * P folded into the exponent (see the producer warp): S4n1 backward -9 % instructions,
+// +0.3 % S4n1 (profiles/r02_experiments.md); 0 restores the unfolded arithmetic
+#ifndef SKR_BWD_SCALE_FOLD
+#define SKR_BWD_SCALE_FOLD 1
+#endif
+constexpr bool kFold = SKR_BWD_SCALE_FOLD;
 constexpr int kComputeThreads = 256;
 
 template <int D>
@@ -230,6 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kPer = BQ / 32;
     float pl[kPer], pd[kPer];
     const float inv_scale = 1.f / a.scale;
+    // kFold: the compute warpgroups produce P' = scale * P (log2(scale) folded into the exponent's
+    // bias: zero extra instructions), so dS' = scale * dS carries dQ's and dK's scale and the dQ
+    // warpgroup stores the accumulator unscaled; dV' = scale * dV is divided once at the epilogue
+    const float ln_scale = kFold ? logf(a.scale) : 0.f;
     auto fetch = [&](const StepIter& s_) {
       const int h = g * grp + s_.hi, q0 = s_.qt * BQ, nv = min(BQ, q_len - q0);
 #pragma unroll
@@ -237,10 +247,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int i = lane + 32 * u;
         const size_t off = (size_t)h * a.ld_lse + cu0 + q0 + i;
         if (C::kInit) {   // accumulator init values: S^T - LSE/scale, dP^T - D
-          pl[u] = i < nv ? -lse[off] * inv_scale : -1e30f;             // p = 0 for invalid queries
+          pl[u] = i < nv ? (ln_scale - lse[off]) * inv_scale : -1e30f;   // p = 0 for invalid queries
           pd[u] = i < nv ? -Dbuf[off] : 0.f;
         } else {
-          pl[u] = i < nv ? lse[off] * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
+          pl[u] = i < nv ? (lse[off] - ln_scale) * 1.4426950408889634f : INFINITY;   // p = 0 for invalid queries
           pd[u] = i < nv ? Dbuf[off] : 0.f;
         }
       }
@@ -613,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : partial         ? (which == 0 ? dk_acc : dv_acc) + row * D
                                              : nullptr;
     const uint32_t tcol = which == 0 ? C::tDK : C::tDV;
-    const float mul = which == 0 ? a.scale : 1.f;
+    const float mul = kFold ? (which == 0 ? 1.f : 1.f / a.scale) : (which == 0 ? a.scale : 1.f);
 #pragma unroll
     for (int c = 0; c < D; c += 32) {
       uint32_t r[32];
@@ -666,6 +676,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->kt_full);
     }
+    // kFold: dS' already carries the scale (the multiply is a no-op the compiler drops)
+    const float dq_mul = kFold ? 1.f : a.scale;
     StepIter it(qt_first, qt_last, grp);
     PhaseAcct pa;   // 0 wait dQ, 1 wait smem tile free, 2 TMEM -> smem, 3 issue reduce
     pa.start();
@@ -700,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int m = 0; m < 8; ++m) off[m] = hb + ((((t % 32) >> 2) ^ m) << 4);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) st_shared_f32(off[q % 8] + q * 128, __uint_as_float(r[hh][q]) * a.scale);
+          for (int q = 0; q < 32; ++q) st_shared_f32(off[q % 8] + q * 128, __uint_as_float(r[hh][q]) * dq_mul);
           fence_async_smem();
           named_bar_sync(1, 128);
           if (warp == 8) {
@@ -730,9 +742,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
-            st_shared_f4(sDQ + (c / 32) * kBoxBytes + sw128_off_f32(t, i), __uint_as_float(r[i]) * a.scale,
-                         __uint_as_float(r[i + 1]) * a.scale, __uint_as_float(r[i + 2]) * a.scale,
-                         __uint_as_float(r[i + 3]) * a.scale);
+            st_shared_f4(sDQ + (c / 32) * kBoxBytes + sw128_off_f32(t, i), __uint_as_float(r[i]) * dq_mul,
+                         __uint_as_float(r[i + 1]) * dq_mul, __uint_as_float(r[i + 2]) * dq_mul,
+                         __uint_as_float(r[i + 3]) * dq_mul);
         }
         tc_fence_before();
         mbar_arrive(&bars->dq_empty);                // TMEM dQ columns may be overwritten

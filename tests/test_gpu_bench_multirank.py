@@ -22,7 +22,9 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("extra,cp,dp", [(["--exchange", "peer"], 2, 1), (["--dp", "2"], 1, 2)])
+@pytest.mark.parametrize("extra,cp,dp", [(["--exchange", "peer"], 2, 1), (["--dp", "2"], 1, 2),
+                                         # the default workload at N = 2 (S4n2: the 128K sequence sharded)
+                                         (["--exchange", "peer", "--config", "S4n2"], 2, 1)])
 def test_bench_two_ranks_one_gpu(extra, cp, dp):
     env = dict(os.environ, SKR_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
@@ -35,3 +37,5 @@ def test_bench_two_ranks_one_gpu(extra, cp, dp):
     j = json.loads(lines[0])
     assert j["n_gpus"] == 2 and j["config"]["cp"] == cp and j["config"]["dp"] == dp
     assert j["value"] > 0 and j["max_mean_rank_time"] >= 1.0 and j["gpu_launches"] > 0
+    if j["config"]["workload"] == "S4n2":
+        assert j["config"]["distributed_seqs"] >= 1 and j["scaling"] == "strong"
