@@ -62,10 +62,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="workload (default: S4n{N}, strong-scaled over the CP group)")
     ap.add_argument("--dp", type=int, default=1, help="DP degree of the DP x CP grid (CP = N / dp)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "peer1"],
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "peer1", "ring"],
                     help="CP exchange: NCCL all-gather / reduce-scatter; 'peer': row f3 step two (peer gather, "
                          "dK/dV reduced from the backward kernel's epilogue into the owners' memory); 'peer1': "
-                         "row f3 step one (peer gather + peer-reduce pass)")
+                         "row f3 step one (peer gather + peer-reduce pass); 'ring': row f4's alternative, ring CP "
+                         "(K/V hop around the CP group point-to-point, partial attentions merged)")
     ap.add_argument("--bwd-band", type=int, default=None,
                     help="query-band height of the backward work items (skr_tiles_bwd; default: the library's)")
     ap.add_argument("--seed", type=int, default=0)
@@ -343,14 +344,16 @@ def run_ours(args):
             comm = sk.PeerComm(cp, cp_rank, group=groups[dp_rank])
         else:
             comm = sk.Comm(cp, cp_rank, group=groups[dp_rank], src=dp_rank * cp)
-    nccl_comm = comm if (comm is not None and args.exchange == "nccl") else None
+    nccl_comm = comm if (comm is not None and args.exchange in ("nccl", "ring")) else None
+    ring = args.exchange == "ring" and comm is not None   # row f4: ring CP (NCCL point-to-point hops)
     side = torch.cuda.Stream(priority=-1)
     main = torch.cuda.current_stream()
     steps = []
     g = torch.Generator(device="cuda")
     # the micro-batches run one after another: their working buffers come from one shared pool
     pool = BufferPool()
-    rsteps = [RankStep(shape, ml, ma, cp, cp_rank, alloc=pool.reserve, band_rows=args.bwd_band) for ml, ma in mbs]
+    rsteps = [RankStep(shape, ml, ma, cp, cp_rank, alloc=pool.reserve, band_rows=args.bwd_band, ring=ring)
+              for ml, ma in mbs]
     pool.materialize()
     for rs in rsteps:
         rs.rebind(pool.get)
@@ -365,7 +368,12 @@ def run_ours(args):
 
     def fwd_bwd(rs, src, ev_do=None, timing=None):
         # ev_do (e2e only): the backward waits for this micro-batch's dO copy, the forward does not
-        if args.exchange in ("peer", "peer1") and comm is not None:
+        if ring:
+            rs.forward_ring(src["q"], src["k"], src["v"], comm, side)
+            if ev_do is not None:
+                torch.cuda.current_stream().wait_event(ev_do)
+            rs.backward_ring(src["do"], comm, side)
+        elif args.exchange in ("peer", "peer1") and comm is not None:
             rs.forward_peer(src["q"], src["k"], src["v"], side)
             if ev_do is not None:
                 torch.cuda.current_stream().wait_event(ev_do)
@@ -413,7 +421,7 @@ def run_ours(args):
     # per-(step, micro-batch) attention timing events (recorded by the library inside the composite
     # steps); created up front so recording them costs nothing in the loop
     K = args.steps
-    use_lib_timing = not (args.exchange in ("peer", "peer1") and comm is not None)
+    use_lib_timing = not (args.exchange in ("peer", "peer1", "ring") and comm is not None)
     timing = None
     if use_lib_timing:
         timing = [[[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(n_mb)] for _ in range(K)]

@@ -163,7 +163,8 @@ typedef struct {                /* one segment class (locals, or distributed chu
   const int32_t* cu_seqlens_q;  /* [n_seg+1] packed query rows */
   const int32_t* q_pos;         /* [n_seg] position of the first query in its sequence */
   const int32_t* k_start;       /* [n_seg] first row of the segment's keys in the K/V buffer */
-  const int32_t* k_len;         /* [n_seg] number of keys = q_pos + q_len */
+  const int32_t* k_len;         /* [n_seg] keys: query i sees keys j < min(k_len, q_pos + i + 1); q_pos + q_len
+                                   for a whole causal segment, less for a ring-CP key chunk (0: none) */
   const int32_t* tiles;         /* work list: [2*n_tiles] from skr_tiles_fwd, [4*n_tiles] from skr_tiles_bwd */
   int32_t n_seg, n_tiles;
   int32_t row_begin, row_end;   /* host ints: the class's packed query rows are [row_begin, row_end) */
@@ -173,7 +174,8 @@ typedef struct {                /* one segment class (locals, or distributed chu
  * [0, n_q_rows) / [0, n_kv_rows) must be finite, also rows no segment owns -- a 128-row tile reads
  * past a segment's end and the tensor cores multiply those rows by exact zeros (0 x NaN = NaN).
  * Forward (row a7; Eq. 2-4): per segment and q-head h (kv head h*hkv/hq),
- * O = softmax(scale QK^T + bottom-right causal mask) V, LSE = natural-log row logsumexp.
+ * O = softmax(scale QK^T + bottom-right causal mask) V, LSE = natural-log row logsumexp; keys at or
+ * past k_len are masked too, and a query that sees no key gets O = 0, LSE = -inf (ring CP partials).
  * q, o: [n_q_rows][hq][d]; k, v: [n_kv_rows][hkv][d]; lse: fp32 [hq][n_q_rows].
  * bf16 in/out with fp32 accumulation (SKR_BF16) or fp32 throughout (SKR_FP32).
  * `tiles` must come from skr_tiles_fwd with block_m = skr_attn_block_m(shape): 128 query rows
@@ -292,6 +294,44 @@ skr_status skr_comm_async_error(skr_comm* c);
  * kernels blocked on the peer) and return SKR_E_NCCL. An aborted communicator rejects further use;
  * skr_comm_destroy still frees it. */
 skr_status skr_comm_wait(skr_comm* c, void* stream, double timeout_s);
+
+/* ------------------------------------------------------------------ row f4: ring CP
+ * The alternative exchange for distributed sequences (ring attention is one of the CP methods
+ * DACP is orthogonal to): instead of all-gathering K/V (R19), each rank's distributed K/V prefix
+ * travels N-1 hops along the ring (skr_comm_ring_shift, point-to-point), and at every hop the rank
+ * computes its own query chunks against the visiting chunk pair as two partial attentions (one per
+ * key chunk of the pair), merged into a running (O, LSE). The backward sends the visiting K/V back
+ * around with fp32 dK/dV accumulators that collect every rank's contribution and arrive home after
+ * N hops; dQ accumulates in fp32 over the hops. Same plans, same packed layout, same kernels.
+ *
+ * Host: segments of ring hop `step` (0..N-1) on `rank` for key-chunk class `cls` (0: chunk s,
+ * 1: chunk 2N-1-s of the visiting pair from rank s = (rank - step) mod N): one segment per own
+ * query chunk in packed-prefix order (cu_seqlens_q covers the rank's dist_rows); k_start indexes
+ * rank s's packed prefix; a key chunk before the query chunk is visible whole (q_pos = its length),
+ * the own chunk is the causal diagonal (q_pos = 0), a later chunk gets k_len = 0 (no visible key).
+ * cap = capacity of q_pos / k_start / k_len (2 * number of distributed sequences needed; cu_seqlens_q
+ * holds cap + 1); SKR_E_CAPACITY sets *n_seg to the need. */
+skr_status skr_ring_segs(const int64_t* mb_lens, const int32_t* assign, int32_t K_mb, int32_t cp, int32_t rank,
+                         int32_t step, int32_t cls, int32_t* cu_seqlens_q, int32_t* q_pos, int32_t* k_start,
+                         int32_t* k_len, int32_t cap, int32_t* n_seg);
+/* Device: merge a partial attention result into the running one, rows [row_begin, row_end), every
+ * q-head: L = log(e^lse_acc + e^lse_part); o_acc = o_acc e^(lse_acc-L) + o_part e^(lse_part-L);
+ * lse_acc = L. o_part: [rows][hq][d] of the shape's dtype (a skr_attn_fwd output); o_acc fp32, same
+ * layout; lse_*: fp32 [hq][ld_lse], natural log; -inf = empty partial (weight 0). first = 1
+ * initialises the running result with the partial. */
+skr_status skr_attn_merge(const skr_attn_shape* s, const void* o_part, const float* lse_part, float* o_acc,
+                          float* lse_acc, int32_t row_begin, int32_t row_end, int32_t ld_lse, int32_t first,
+                          void* stream);
+/* Device: backward of one segment class with every gradient an fp32 accumulator the caller owns and
+ * zeroes: dq [n_q_rows][hq][d], dk / dv [n_kv_rows][hkv][d] are ADDED to (o / lse: the merged final
+ * forward results). Otherwise as skr_attn_bwd. */
+skr_status skr_attn_bwd_acc(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k, const void* v,
+                            const void* o, const void* dout, const float* lse, float* dq, float* dk, float* dv,
+                            int32_t n_q_rows, int32_t n_kv_rows, void* ws, size_t ws_bytes, void* stream);
+/* One ring hop: send_bufs[i] (bytes[i]) to rank + 1, receive rank - 1's into recv_bufs[i], one NCCL
+ * group on `stream` (a 1-rank communicator sends to itself). */
+skr_status skr_comm_ring_shift(skr_comm* c, const void* const* send_bufs, void* const* recv_bufs,
+                               const size_t* bytes, int32_t n_bufs, void* stream);
 
 /* ------------------------------------------------------------------ a5-a9 as one call per direction
  * The CP-rank step of one micro-batch (Eq. 2, mirrored for the

@@ -11,8 +11,8 @@ skr_status sm100_attn_fwd(const AttnArgs& a, int d, const void* q, const void* k
                           int n_q_rows, int n_kv_rows, cudaStream_t st);
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
                           const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
-                          void* dv, int accumulate, float* Dbuf, float* dq_acc, float* dk_acc, float* dv_acc,
-                          int n_q_rows, int n_kv_rows, cudaStream_t st);
+                          void* dv, int accumulate, int dq_accumulate, float* Dbuf, float* dq_acc, float* dk_acc,
+                          float* dv_acc, int n_q_rows, int n_kv_rows, cudaStream_t st);
 
 // Query-banded backward work items (skr_tiles_bwd): the bands of one key tile each add an fp32
 // partial dK / dV into an accumulator (ws) -- zeroed before the backward kernel and cast into dk / dv
@@ -41,6 +41,39 @@ __global__ void __launch_bounds__(256) band_kv_kernel(AttnArgs a, int bn, int d,
       reinterpret_cast<float4*>(dv)[e] = reinterpret_cast<const float4*>(dv_acc)[e];
     }
   }
+}
+
+// Ring CP (row f4): merge one partial attention result (O_p normalised, LSE_p natural log) into
+// the running one (O_a fp32, LSE_a): L = log(e^LSE_a + e^LSE_p), O_a <- O_a e^(LSE_a - L) + O_p
+// e^(LSE_p - L), LSE_a <- L -- the plain identity softmax over a union of disjoint key sets obeys.
+// LSE = -inf marks an empty partial (weight 0). One warp per (row, head): the lanes read LSE_a before
+// lane 0 overwrites it.
+template <typename T>
+__global__ void __launch_bounds__(256) merge_kernel(const T* __restrict__ o_p, const float* __restrict__ lse_p,
+                                                    float* __restrict__ o_a, float* __restrict__ lse_a, int row_begin,
+                                                    int row_end, int hq, int d, int ld, int first) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= (int64_t)(row_end - row_begin) * hq) return;
+  const int row = row_begin + (int)(w / hq), h = (int)(w % hq);
+  const size_t lo = (size_t)h * ld + row, base = ((size_t)row * hq + h) * d;
+  const float lp = lse_p[lo];
+  float wa = 0.f, wp = 1.f, L = lp;
+  if (!first) {
+    const float la = lse_a[lo];
+    const float mx = fmaxf(la, lp);
+    if (mx == -INFINITY) return;                          // both empty: O_a stays 0, LSE_a -inf
+    wa = expf(la - mx), wp = expf(lp - mx);
+    const float den = wa + wp;                            // >= 1
+    wa /= den, wp /= den;
+    L = mx + logf(den);
+  }
+  for (int c = lane; c < d; c += 32) {
+    const float x = (float)o_p[base + c];
+    o_a[base + c] = first ? x : o_a[base + c] * wa + x * wp;
+  }
+  __syncwarp();
+  if (lane == 0) lse_a[lo] = L;
 }
 
 static skr_status band_kv(const AttnArgs& a, int bn, int d, int convert, float* dk_acc, float* dv_acc, void* dk,
@@ -110,6 +143,27 @@ SKR_EXPORT size_t skr_attn_bwd_ws_bytes(const skr_attn_shape* s, int32_t n_q_row
   return ws_kv_off(s, n_q_rows) + 2 * ws_kv_bytes(s, n_q_rows);
 }
 
+SKR_EXPORT skr_status skr_attn_merge(const skr_attn_shape* s, const void* o_part, const float* lse_part, float* o_acc,
+                                     float* lse_acc, int32_t row_begin, int32_t row_end, int32_t ld_lse, int32_t first,
+                                     void* stream) {
+  if (skr_status e = check_shape(s)) return e;
+  SKR_REQUIRE(row_begin >= 0 && row_begin <= row_end && row_end <= ld_lse, "skr_attn_merge: rows [%d,%d) / ld %d",
+              row_begin, row_end, ld_lse);
+  if (row_end == row_begin) return SKR_OK;
+  SKR_REQUIRE(o_part && lse_part && o_acc && lse_acc, "skr_attn_merge: null pointer");
+  if (skr_status e = check_sm100()) return e;
+  const int64_t warps = (int64_t)(row_end - row_begin) * s->hq;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (s->dtype == SKR_BF16)
+    merge_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)o_part, lse_part, o_acc, lse_acc,
+                                                        row_begin, row_end, s->hq, s->d, ld_lse, first);
+  else
+    merge_kernel<float><<<blocks, 256, 0, st>>>((const float*)o_part, lse_part, o_acc, lse_acc, row_begin, row_end,
+                                                s->hq, s->d, ld_lse, first);
+  return launch_status("attn merge");
+}
+
 SKR_EXPORT skr_status skr_attn_fwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
                                    const void* v, void* o, float* lse, int32_t n_q_rows, int32_t n_kv_rows,
                                    void* stream) {
@@ -130,7 +184,7 @@ static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, cons
                                 const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
                                 void* dv, int32_t kv_accumulate, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
                                 size_t ws_bytes, void* stream, const uint64_t* peer_dk, const uint64_t* peer_dv,
-                                const int32_t* row_map, int32_t pad_P);
+                                const int32_t* row_map, int32_t pad_P, int32_t dq_accumulate = 0);
 
 SKR_EXPORT skr_status skr_attn_bwd(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
                                    const void* v, const void* o, const void* dout, const float* lse, void* dq,
@@ -139,6 +193,16 @@ SKR_EXPORT skr_status skr_attn_bwd(const skr_attn_shape* s, const skr_segs* g, c
   SKR_REQUIRE(kv_accumulate == 0 || kv_accumulate == 1, "skr_attn_bwd: kv_accumulate must be 0 or 1");
   return attn_bwd_impl(s, g, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate, n_q_rows, n_kv_rows, ws, ws_bytes,
                        stream, nullptr, nullptr, nullptr, 0);
+}
+
+// Ring CP (row f4): every gradient is an fp32 accumulator the caller owns and zeroes; the call adds
+// this segment class's contribution (dq [n_q_rows][hq][d], dk / dv [n_kv_rows][hkv][d], all fp32).
+SKR_EXPORT skr_status skr_attn_bwd_acc(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
+                                       const void* v, const void* o, const void* dout, const float* lse, float* dq,
+                                       float* dk, float* dv, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
+                                       size_t ws_bytes, void* stream) {
+  return attn_bwd_impl(s, g, q, k, v, o, dout, lse, dq, dk, dv, 1, n_q_rows, n_kv_rows, ws, ws_bytes, stream, nullptr,
+                       nullptr, nullptr, 0, 1);
 }
 
 SKR_EXPORT skr_status skr_attn_bwd_peer(const skr_attn_shape* s, const skr_segs* g, const void* q, const void* k,
@@ -156,7 +220,7 @@ static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, cons
                                 const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
                                 void* dv, int32_t kv_accumulate, int32_t n_q_rows, int32_t n_kv_rows, void* ws,
                                 size_t ws_bytes, void* stream, const uint64_t* peer_dk, const uint64_t* peer_dv,
-                                const int32_t* row_map, int32_t pad_P) {
+                                const int32_t* row_map, int32_t pad_P, int32_t dq_accumulate) {
   if (skr_status e = check_shape(s)) return e;
   SKR_REQUIRE(g && n_q_rows >= 0 && n_kv_rows >= 0, "skr_attn_bwd: bad segments / sizes");
   SKR_REQUIRE(g->row_begin >= 0 && g->row_begin <= g->row_end && g->row_end <= n_q_rows,
@@ -187,11 +251,11 @@ static skr_status attn_bwd_impl(const skr_attn_shape* s, const skr_segs* g, cons
   if (!bf16) {
     e = simt_attn_bwd(a, s->d, g->row_begin, g->row_end, (const float*)q, (const float*)k, (const float*)v,
                       (const float*)o, (const float*)dout, lse, (float*)dq, (float*)dk, (float*)dv, kv_accumulate,
-                      Dbuf, dk_acc, dv_acc, st);
+                      dq_accumulate, Dbuf, dk_acc, dv_acc, st);
   } else {
     float* dq_acc = (float*)((uint8_t*)ws + ws_dq_off(s, n_q_rows));
-    e = sm100_attn_bwd(a, s->d, g->row_begin, g->row_end, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate, Dbuf,
-                       dq_acc, dk_acc, dv_acc, n_q_rows, n_kv_rows, st);
+    e = sm100_attn_bwd(a, s->d, g->row_begin, g->row_end, q, k, v, o, dout, lse, dq, dk, dv, kv_accumulate,
+                       dq_accumulate, Dbuf, dq_acc, dk_acc, dv_acc, n_q_rows, n_kv_rows, st);
   }
   if (e) return e;
   if (kv_accumulate == 0) return band_kv(a, bn, s->d, 1, dk_acc, dv_acc, dk, dv, bf16, st);

@@ -489,7 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int n = 0; n < n_steps; ++n, it.next()) {
       const int st = n % C::kStages;
       const int qp_base = q_pos + it.qt * BQ + col0;        // position of this warpgroup's first query
-      const bool diag = kv0 + BN - 1 > qp_base;             // warp-uniform: causal mask needed
+      // warp-uniform: causal mask needed, or the tile holds keys past k_len (invisible: ring CP)
+      const bool diag = kv0 + BN - 1 > qp_base || kv0 + BN > k_len;
       mbar_wait(&bars->qdo_full[st], (n / C::kStages) & 1);
       if (threadIdx.x == 0) trace(14);
       const uint32_t a_lse = sAux + (st * BQ + col0) * 4, a_dd = sAux + (C::kStages * BQ + st * BQ + col0) * 4;
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (diag) {
 #pragma unroll
         for (int i = 0; i < H; ++i)
-          if (kvp > qp_base + i) p[i] = 0.f;               // causal (invalid queries: lse2 = +inf -> 0)
+          if (kvp > qp_base + i || kvp >= k_len) p[i] = 0.f;   // causal (invalid queries: lse2 = +inf -> 0)
       }
       pa.mark(2);
       if (n > 0) mbar_wait(&bars->dv_done, (n - 1) & 1);     // P^T TMEM columns free
@@ -844,8 +845,11 @@ extern "C" __attribute__((visibility("default"))) int skr_debug_bwd_trace(unsign
 
 skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const void* q, const void* k,
                           const void* v, const void* o, const void* dout, const float* lse, void* dq, void* dk,
-                          void* dv, int accumulate, float* Dbuf, float* dq_acc, float* dk_acc, float* dv_acc,
-                          int n_q_rows, int n_kv_rows, cudaStream_t st) {
+                          void* dv, int accumulate, int dq_accumulate, float* Dbuf, float* dq_acc, float* dk_acc,
+                          float* dv_acc, int n_q_rows, int n_kv_rows, cudaStream_t st) {
+  // dq_accumulate (ring CP): dq is the caller's fp32 accumulator -- the kernel reduce-adds into it
+  // directly, no zeroing and no bf16 conversion here
+  if (dq_accumulate) dq_acc = static_cast<float*>(dq);
   trace_buffer();
   if (d != 64 && d != 128) return fail(SKR_E_UNSUPPORTED, "bf16 backward supports d in {64,128}");
   const int rows = row_end - row_begin;
@@ -859,7 +863,8 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
       bwd::preprocess_kernel<64><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, (const __nv_bfloat16*)o,
                                                          (const __nv_bfloat16*)dout, Dbuf, a.ld_lse);
     if (skr_status e = launch_status("attn bwd preprocess")) return e;
-    if (cudaMemsetAsync(dq_acc + (size_t)row_begin * a.hq * d, 0, (size_t)rows * a.hq * d * 4, st) != cudaSuccess)
+    if (!dq_accumulate &&
+        cudaMemsetAsync(dq_acc + (size_t)row_begin * a.hq * d, 0, (size_t)rows * a.hq * d * 4, st) != cudaSuccess)
       return fail(SKR_E_CUDA, "attn bwd: dQ accumulator memset");
   }
   if (a.n_tiles > 0) {
@@ -906,7 +911,7 @@ skr_status sm100_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, 
     }
     if (skr_status e = launch_status("attn_bwd_kernel")) return e;
   }
-  if (rows > 0) {
+  if (rows > 0 && !dq_accumulate) {
     const int64_t b4 = (int64_t)row_begin * a.hq * d / 4, e4 = (int64_t)row_end * a.hq * d / 4;
     const int blocks = (int)std::min<int64_t>((e4 - b4 + 255) / 256, 148 * 16);
     bwd::convert_dq_kernel<<<blocks, 256, 0, st>>>((const float4*)dq_acc, (uint2*)dq, b4, e4);

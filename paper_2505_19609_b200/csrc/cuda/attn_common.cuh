@@ -38,6 +38,7 @@ skr_status simt_attn_fwd(const AttnArgs& a, int d, const float* q, const float* 
                          float* lse, cudaStream_t st);
 skr_status simt_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const float* q, const float* k,
                          const float* v, const float* o, const float* dout, const float* lse, float* dq, float* dk,
-                         float* dv, int accumulate, float* Dbuf, float* dk_acc, float* dv_acc, cudaStream_t st);
+                         float* dv, int accumulate, int dq_accumulate, float* Dbuf, float* dk_acc, float* dv_acc,
+                         cudaStream_t st);
 
 }  // namespace skr

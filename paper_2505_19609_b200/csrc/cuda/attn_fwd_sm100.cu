@@ -77,6 +77,21 @@ __device__ __forceinline__ void trace_smw(int, int) {}
 #endif
 
 constexpr int BM = 128, BN = 128;
+
+// A tile whose queries see no key at all (ring CP: a key chunk after the query chunk, k_len = 0):
+// O = 0 and LSE = -inf, the neutral element of the partial-attention merge. Written by the whole CTA
+// before any barrier / TMEM is set up; the caller returns right after (the condition is CTA-uniform).
+template <int D>
+__device__ __forceinline__ void store_empty_tile(const AttnArgs& a, __nv_bfloat16* __restrict__ out,
+                                                 float* __restrict__ lse, int r0, int n_valid, int h0, int nh) {
+  const int per_row = nh * (D / 8);                     // 16-byte vectors per query row
+  for (int e = threadIdx.x; e < n_valid * per_row; e += blockDim.x) {
+    const int row = e / per_row, rem = e % per_row, hh = rem / (D / 8), c = rem % (D / 8);
+    *reinterpret_cast<uint4*>(out + ((size_t)(r0 + row) * a.hq + h0 + hh) * D + c * 8) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (int e = threadIdx.x; e < n_valid * nh; e += blockDim.x)
+    lse[(size_t)(h0 + e / n_valid) * a.ld_lse + r0 + e % n_valid] = -INFINITY;
+}
 constexpr int kThreads = 576;
 // Grid order of the two-head kernel (launch argument head_major): 0 = (head pair, tile) with the
 // pair fastest; 1 = (tile, head pair), every tile of one pair before the next pair, so the CTAs in
@@ -180,10 +195,15 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
   const int r0 = cu0 + tile * BM;                       // first packed query row of the tile
   const int n_valid = min(BM, cu1 - r0);
   const int qp0 = a.q_pos[seg] + tile * BM;             // position of the tile's first query
-  const int k_hi = qp0 + n_valid;                       // keys visible to the last valid query
-  const int n_kv = (k_hi + BN - 1) / BN;
+  const int k_len = a.k_len[seg];                       // keys past k_len are invisible (ring CP)
+  const int k_hi = min(qp0 + n_valid, k_len);           // keys visible to the last valid query
+  const int n_kv = (max(k_hi, 0) + BN - 1) / BN;
   const int kst = a.k_start[seg];
   const int nq = hb >= 0 ? 2 : 1;
+  if (n_kv == 0) {
+    store_empty_tile<D>(a, out, lse, r0, n_valid, ha, nq);
+    return;
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
@@ -430,10 +450,10 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         }
         pa.mark(1);
         const int kv0 = j * BN;
-        if (kv0 + BN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
+        if (kv0 + BN - 1 > qp0 || kv0 + BN > k_len) {   // diagonal / last tile: mask keys after the query
 #pragma unroll
           for (int i = 0; i < BN; ++i)
-            if (kv0 + i > qp) x[i] = -INFINITY;
+            if (kv0 + i > qp || kv0 + i >= k_len) x[i] = -INFINITY;
         }
         float mxs[8];
 #pragma unroll
@@ -623,10 +643,10 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         }
         pa.mark(1);
         const int kv0 = j * BN + hf * HN;
-        if (kv0 + HN - 1 > qp0) {             // diagonal tile(s): mask keys after the query
+        if (kv0 + HN - 1 > qp0 || kv0 + HN > k_len) {   // diagonal / last tile: mask keys after the query
 #pragma unroll
           for (int i = 0; i < HN; ++i)
-            if (kv0 + i > qp) x[i] = -INFINITY;
+            if (kv0 + i > qp || kv0 + i >= k_len) x[i] = -INFINITY;
         }
         // half-row max: 8 independent chains of three-input max, then combine with the other half
         float mxs[8];
@@ -780,8 +800,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int r0 = cu0 + tile * BM;
   const int n_valid = min(BM, cu1 - r0);
   const int qp0 = a.q_pos[seg] + tile * BM;
-  const int n_kv = (qp0 + n_valid + BN - 1) / BN;
+  const int k_len = a.k_len[seg];
+  const int n_kv = (max(min(qp0 + n_valid, k_len), 0) + BN - 1) / BN;
   const int kst = a.k_start[seg];
+  if (n_kv == 0) {
+    store_empty_tile<128>(a, out, lse, r0, n_valid, h, 1);
+    return;
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
@@ -890,10 +915,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars->s_free[b]);          // S buffer b may take S(j + 2)
       const int kv0 = j * BN + w * HN;
-      if (kv0 + HN - 1 > qp0) {
+      if (kv0 + HN - 1 > qp0 || kv0 + HN > k_len) {
 #pragma unroll
         for (int i = 0; i < HN; ++i)
-          if (kv0 + i > qp) x[i] = -INFINITY;
+          if (kv0 + i > qp || kv0 + i >= k_len) x[i] = -INFINITY;
       }
       float mxs[8];
 #pragma unroll
@@ -1038,11 +1063,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int cu0 = a.cu[seg], cu1 = a.cu[seg + 1];
   const int rs0 = cu0 + tile0 * BM;                     // first row of the super tile
   const int n_valid_pair = min(2 * BM, cu1 - rs0);
-  const int n_kv = (a.q_pos[seg] + tile0 * BM + n_valid_pair + BN - 1) / BN;   // same in both CTAs
+  const int k_len = a.k_len[seg];
+  const int n_kv = (max(min(a.q_pos[seg] + tile0 * BM + n_valid_pair, k_len), 0) + BN - 1) / BN;   // same in both CTAs
   const int r0 = rs0 + (int)rank * BM;                  // this CTA's rows
   const int n_valid = min(BM, cu1 - r0);               // may be <= 0 for rank 1
   const int qp0 = a.q_pos[seg] + (tile0 + (int)rank) * BM;
   const int kst = a.k_start[seg];
+  if (n_kv == 0) {                                      // both CTAs of the pair (n_kv is shared)
+    store_empty_tile<128>(a, out, lse, r0, max(n_valid, 0), h, 1);
+    return;
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
@@ -1159,10 +1189,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(s_free_l[b]);   // S buffer b may take S(j + 2)
       const int kv0 = j * BN + w * HN;
-      if (kv0 + HN - 1 > qp0) {
+      if (kv0 + HN - 1 > qp0 || kv0 + HN > k_len) {
 #pragma unroll
         for (int i = 0; i < HN; ++i)
-          if (kv0 + i > qp) x[i] = -INFINITY;
+          if (kv0 + i > qp || kv0 + i >= k_len) x[i] = -INFINITY;
       }
       float mxs[8];
 #pragma unroll

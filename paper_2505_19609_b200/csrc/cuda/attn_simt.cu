@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(256) fwd_kernel(AttnArgs a, const float* __res
       acc[i][e] = 0.f;
     }
   }
-  const int n_keys = qpos + (r_first - cu0) + n_rows;  // keys visible to the last row
+  // keys visible to the last row; keys past k_len are invisible (ring CP)
+  const int n_keys = min(qpos + (r_first - cu0) + n_rows, a.k_len[seg]);
   for (int kb = 0; kb < n_keys; kb += kBN) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < kBN * D; idx += blockDim.x) {
@@ -90,10 +91,11 @@ __global__ void __launch_bounds__(256) fwd_kernel(AttnArgs a, const float* __res
     const int rr = warp * kRowsPerWarp + i;
     if (rr >= n_rows) continue;
     const size_t row = r_first + rr;
-    const float inv = 1.f / l[i];
+    // a row that sees no key (ring CP): O = 0, LSE = -inf (the merge's neutral element)
+    const float inv = l[i] > 0.f ? 1.f / l[i] : 0.f;
 #pragma unroll
     for (int e = 0; e < E; ++e) o[(row * a.hq + h) * D + lane + 32 * e] = acc[i][e] * inv;
-    if (lane == 0) lse[(size_t)h * a.ld_lse + row] = m[i] + logf(l[i]);
+    if (lane == 0) lse[(size_t)h * a.ld_lse + row] = l[i] > 0.f ? m[i] + logf(l[i]) : -INFINITY;
   }
 }
 
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(256) bwd_dq_kernel(AttnArgs a, int row_begin, 
                                                      const float* __restrict__ q, const float* __restrict__ k,
                                                      const float* __restrict__ v, const float* __restrict__ dout,
                                                      const float* __restrict__ lse, const float* __restrict__ Dbuf,
-                                                     float* __restrict__ dq) {
+                                                     float* __restrict__ dq, int dq_accumulate) {
   constexpr int E = D / 32;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   const int row = row_begin + gw / a.hq, h = gw % a.hq;
@@ -141,7 +143,8 @@ __global__ void __launch_bounds__(256) bwd_dq_kernel(AttnArgs a, int row_begin, 
     acc[e] = 0.f;
   }
   const float L = lse[(size_t)h * a.ld_lse + row], Di = Dbuf[(size_t)h * a.ld_lse + row];
-  for (int j = 0; j <= pos; ++j) {
+  const int j_end = min(pos + 1, a.k_len[seg]);
+  for (int j = 0; j < j_end; ++j) {
     const size_t ko = ((size_t)(a.k_start[seg] + j) * a.hkv + g) * D;
     float s = 0.f, dp = 0.f;
 #pragma unroll
@@ -157,7 +160,10 @@ __global__ void __launch_bounds__(256) bwd_dq_kernel(AttnArgs a, int row_begin, 
     for (int e = 0; e < E; ++e) acc[e] += ds * k[ko + lane + 32 * e];
   }
 #pragma unroll
-  for (int e = 0; e < E; ++e) dq[((size_t)row * a.hq + h) * D + lane + 32 * e] = acc[e] * a.scale;
+  for (int e = 0; e < E; ++e) {
+    float* d = dq + ((size_t)row * a.hq + h) * D + lane + 32 * e;
+    *d = dq_accumulate ? *d + acc[e] * a.scale : acc[e] * a.scale;   // accumulate: ring CP steps
+  }
 }
 
 // dK, dV: one warp per (key row, kv head), loop over the group's heads and the queries that see it.
@@ -254,19 +260,20 @@ skr_status simt_attn_fwd(const AttnArgs& a, int d, const float* q, const float* 
 
 skr_status simt_attn_bwd(const AttnArgs& a, int d, int row_begin, int row_end, const float* q, const float* k,
                          const float* v, const float* o, const float* dout, const float* lse, float* dq, float* dk,
-                         float* dv, int accumulate, float* Dbuf, float* dk_acc, float* dv_acc, cudaStream_t st) {
+                         float* dv, int accumulate, int dq_accumulate, float* Dbuf, float* dk_acc, float* dv_acc,
+                         cudaStream_t st) {
   if (row_end > row_begin) {
     const int warps = (row_end - row_begin) * a.hq;
     const int blocks = (warps * 32 + 255) / 256;
     if (d == 64) {
       simt::bwd_pre_kernel<64><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, o, dout, Dbuf, a.ld_lse);
-      simt::bwd_dq_kernel<64><<<blocks, 256, 0, st>>>(a, row_begin, row_end, q, k, v, dout, lse, Dbuf, dq);
+      simt::bwd_dq_kernel<64><<<blocks, 256, 0, st>>>(a, row_begin, row_end, q, k, v, dout, lse, Dbuf, dq, dq_accumulate);
     } else if (d == 128) {
       simt::bwd_pre_kernel<128><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, o, dout, Dbuf, a.ld_lse);
-      simt::bwd_dq_kernel<128><<<blocks, 256, 0, st>>>(a, row_begin, row_end, q, k, v, dout, lse, Dbuf, dq);
+      simt::bwd_dq_kernel<128><<<blocks, 256, 0, st>>>(a, row_begin, row_end, q, k, v, dout, lse, Dbuf, dq, dq_accumulate);
     } else if (d == 32) {
       simt::bwd_pre_kernel<32><<<blocks, 256, 0, st>>>(row_begin, row_end, a.hq, o, dout, Dbuf, a.ld_lse);
-      simt::bwd_dq_kernel<32><<<blocks, 256, 0, st>>>(a, row_begin, row_end, q, k, v, dout, lse, Dbuf, dq);
+      simt::bwd_dq_kernel<32><<<blocks, 256, 0, st>>>(a, row_begin, row_end, q, k, v, dout, lse, Dbuf, dq, dq_accumulate);
     } else {
       return fail(SKR_E_UNSUPPORTED, "fp32 mode supports d in {32, 64, 128}");
     }

@@ -125,3 +125,27 @@ SKR_EXPORT skr_status skr_comm_all_reduce_f32(skr_comm* c, float* buf, size_t co
   return nccl_status(ncclAllReduce(buf, buf, count, ncclFloat, ncclSum, c->comm, (cudaStream_t)stream),
                      "ncclAllReduce");
 }
+
+// Ring CP (row f4's alternative exchange): one ring hop -- every buffer i is sent to rank + 1
+// and recv_bufs[i] receives rank - 1's buffer i, all in one NCCL group (point-to-point over NVLink,
+// no collective). A 1-rank communicator sends to itself.
+SKR_EXPORT skr_status skr_comm_ring_shift(skr_comm* c, const void* const* send_bufs, void* const* recv_bufs,
+                                          const size_t* bytes, int32_t n_bufs, void* stream) {
+  SKR_REQUIRE(c && c->comm && n_bufs >= 0 && (n_bufs == 0 || (send_bufs && recv_bufs && bytes)),
+              "skr_comm_ring_shift: bad arguments");
+  const int next = (c->rank + 1) % c->nranks, prev = (c->rank - 1 + c->nranks) % c->nranks;
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (skr_status s = nccl_status(ncclGroupStart(), "ncclGroupStart")) return s;
+  for (int32_t i = 0; i < n_bufs; ++i) {
+    if (bytes[i] == 0) continue;
+    if (skr_status s = nccl_status(ncclSend(send_bufs[i], bytes[i], ncclUint8, next, c->comm, st), "ncclSend")) {
+      ncclGroupEnd();
+      return s;
+    }
+    if (skr_status s = nccl_status(ncclRecv(recv_bufs[i], bytes[i], ncclUint8, prev, c->comm, st), "ncclRecv")) {
+      ncclGroupEnd();
+      return s;
+    }
+  }
+  return nccl_status(ncclGroupEnd(), "ncclGroupEnd");
+}

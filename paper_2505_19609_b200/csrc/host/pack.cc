@@ -175,6 +175,54 @@ SKR_EXPORT skr_status skr_pack_chunks(const int64_t* L, const int32_t* A, int32_
   return SKR_OK;
 }
 
+// Ring CP (row f4's alternative exchange): ring step `step` on rank j computes its own
+// distributed query chunks against the K / V prefix of rank s = (j - step) mod N, which has travelled
+// `step` hops along the ring. One segment per own query chunk (prefix order, so cu_seqlens_q tiles the
+// rank's distributed prefix rows), against ONE key chunk of the visiting pair: cls 0 -> chunk s,
+// cls 1 -> chunk 2N-1-s. Zigzag chunks are disjoint position ranges, so a key chunk before the query
+// chunk is visible whole (q_pos = its length: every key precedes every query), the same chunk is the
+// plain causal diagonal (q_pos = 0, only at step 0), a later chunk is invisible (k_len = 0: the
+// attention calls write O = 0, LSE = -inf there). Over the N steps and both classes every key chunk
+// c' <= c of a query chunk c is visited exactly once (see tests/test_host_planner.py).
+SKR_EXPORT skr_status skr_ring_segs(const int64_t* L, const int32_t* A, int32_t K, int32_t N, int32_t j,
+                                    int32_t step, int32_t cls, int32_t* cu_seqlens_q, int32_t* q_pos,
+                                    int32_t* k_start, int32_t* k_len, int32_t cap, int32_t* n_seg) {
+  SKR_REQUIRE(N >= 1 && j >= 0 && j < N && step >= 0 && step < N && (cls == 0 || cls == 1) && n_seg,
+              "skr_ring_segs: bad rank / step / class");
+  MbView v;
+  if (skr_status st = view(L, A, K, N, &v)) return st;
+  *n_seg = (int32_t)(2 * v.dist.size());
+  if (*n_seg > cap) return fail(SKR_E_CAPACITY, "skr_ring_segs: need %d segments", *n_seg);
+  SKR_REQUIRE(cu_seqlens_q && q_pos && k_start && k_len, "skr_ring_segs: null output");
+  const int32_t s = ((j - step) % N + N) % N;
+  const int32_t ck = cls == 0 ? s : 2 * N - 1 - s;
+  int64_t qrow = 0, krow = 0;   // row in rank j's prefix / in the visiting (rank s's) prefix
+  int32_t seg = 0;
+  cu_seqlens_q[0] = 0;
+  for (int32_t k : v.dist) {
+    // key chunk ck's rows inside rank s's prefix (chunk s first, then 2N-1-s)
+    const Chunk ks = chunk_of(L[k], s, N), kx = chunk_of(L[k], ck, N);
+    const int64_t koff = krow + (ck == s ? 0 : ks.b - ks.a);
+    const int64_t lk = kx.b - kx.a;
+    for (int32_t c : {j, 2 * N - 1 - j}) {
+      const Chunk q = chunk_of(L[k], c, N);
+      const int64_t lq = q.b - q.a;
+      if (lk == 0 || ck > c) {             // invisible
+        q_pos[seg] = 0, k_start[seg] = 0, k_len[seg] = 0;
+      } else if (ck < c) {                 // every key before every query
+        q_pos[seg] = (int32_t)lk, k_start[seg] = (int32_t)koff, k_len[seg] = (int32_t)lk;
+      } else {                             // the causal diagonal of the rank's own chunk
+        q_pos[seg] = 0, k_start[seg] = (int32_t)koff, k_len[seg] = (int32_t)lk;
+      }
+      qrow += lq;
+      cu_seqlens_q[++seg] = (int32_t)qrow;
+    }
+    const Chunk k2 = chunk_of(L[k], 2 * N - 1 - s, N);
+    krow += (ks.b - ks.a) + (k2.b - k2.a);
+  }
+  return SKR_OK;
+}
+
 namespace {
 
 struct Tile {

@@ -63,10 +63,12 @@ def _alloc_new(device):
 
 
 class RankStep:
-    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda", alloc=None, band_rows=None):
+    def __init__(self, shape, mb_lens, assign, cp: int, rank: int, device="cuda", alloc=None, band_rows=None,
+                 ring=False):
         """alloc(name, shape, dtype) -> tensor: where the working buffers come from (default: fresh
         allocations; BufferPool.reserve to share them across micro-batches). band_rows: query-band
-        height of the backward work lists (skr_tiles_bwd; None = the library's choice)."""
+        height of the backward work lists (skr_tiles_bwd; None = the library's choice). ring: also build
+        the tables and buffers of the ring-CP exchange (row f4, forward_ring / backward_ring)."""
         self.shape, self.cp, self.rank = shape, cp, rank
         self.dev = device
         self._alloc = alloc or _alloc_new(device)
@@ -121,6 +123,31 @@ class RankStep:
             # prefix); every rank's backward red-adds its partials into them over peer memory
             for name in ("dk_acc", "dv_acc"):
                 self._buf(name, (max(P, 1), hkv, d), f32)
+        self.ring = bool(ring) and self.has_dist
+        if self.ring:
+            # row f4, ring CP: per hop r and key-chunk class c the segment tables of this rank's query
+            # chunks against the visiting prefix (skr_ring_segs), double-buffered visiting K/V and
+            # travelling fp32 dK/dV accumulators, the partial O / LSE and the fp32 running O, dQ
+            P = max(self.P, 1)
+            self.ring_f, self.ring_b = [], []
+            for r in range(cp):
+                fr, br = [], []
+                for c in (0, 1):
+                    t = sk.skr_ring_segs(mb_lens, assign, cp, rank, r, c)
+                    fr.append(sk.make_segs(shape, t["cu_seqlens_q"], t["q_pos"], t["k_start"], t["k_len"], "fwd",
+                                           device))
+                    br.append(sk.make_segs(shape, t["cu_seqlens_q"], t["q_pos"], t["k_start"], t["k_len"], "bwd",
+                                           device, band_rows))
+                self.ring_f.append(fr)
+                self.ring_b.append(br)
+            for name in ("ring_k0", "ring_k1", "ring_v0", "ring_v1"):
+                self._buf(name, (P, hkv, d), dt)
+            for name in ("ring_dk0", "ring_dk1", "ring_dv0", "ring_dv1"):
+                self._buf(name, (P, hkv, d), f32)
+            self._buf("ring_o", (R, hq, d), dt)
+            self._buf("ring_lse", (hq, R), f32)
+            self._buf("ring_oacc", (R, hq, d), f32)
+            self._buf("ring_dq", (R, hq, d), f32)
 
     def cp_step(self, q_src, k_src, v_src, do_src, timing=None):
         """The skr_cp_step of this micro-batch (row a5-a9 composite C-ABI call) for these inputs.
@@ -170,6 +197,16 @@ class RankStep:
         if self.has_dist:
             dist_rows = self.dist_b.row_end - self.dist_b.row_begin
             n += (self.dist_f.n_tiles > 0) + (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)
+            if exchange == "ring" and self.ring:
+                # replaces the all-gather path's distributed launches: per hop and key-chunk class a
+                # forward + merge, a D-preprocess + backward (accumulate mode: no dQ convert, no band
+                # zero / cast); then the casts of O, dQ, dK, dV
+                n -= (self.dist_f.n_tiles > 0) + (self.dist_b.n_tiles > 0) + 2 * (dist_rows > 0)
+                for r in range(self.cp):
+                    for c in (0, 1):
+                        n += (self.ring_f[r][c].n_tiles > 0) + 2 * (dist_rows > 0) + (self.ring_b[r][c].n_tiles > 0)
+                n += 4 * (dist_rows > 0 and self.dt != torch.float32)
+                return n
             if exchange == "peer":
                 # step two: gather K, V; cast dK, dV (the reduction is inside the bwd kernel); 3 signal + wait
                 n += 2 + 2 * (self.dist_rows > 0) + 3 * 2
@@ -305,6 +342,148 @@ class RankStep:
         if self.has_dist:
             main.wait_event(ev_rs)
 
+
+    # ------------------------------------------------------------------ row f4: ring CP
+    def ring_bufs(self, r):
+        """Visiting K / V buffers of hop r >= 1 (double-buffered; hop 0 visits the own prefix)."""
+        i = (r - 1) % 2
+        return getattr(self, f"ring_k{i}"), getattr(self, f"ring_v{i}")
+
+    def ring_acc(self, r):
+        """Travelling fp32 dK / dV accumulators of hop r (double-buffered)."""
+        i = r % 2
+        return getattr(self, f"ring_dk{i}"), getattr(self, f"ring_dv{i}")
+
+    def ring_fwd_hop(self, r, vk, vv, stream=None):
+        """Hop r of the ring forward: this rank's query chunks against the visiting prefix (vk, vv),
+        one partial attention per key chunk of the pair, each merged into the running (O, LSE)."""
+        n = self.dist_rows
+        for c in (0, 1):
+            self._timed("fwd_dist", lambda c=c: sk.skr_attn_fwd(self.shape, self.ring_f[r][c], self.q, vk, vv,
+                                                              self.ring_o, self.ring_lse, stream), stream)
+            sk.skr_attn_merge(self.shape, self.ring_o, self.ring_lse, self.ring_oacc, self.lse, 0, n,
+                              r == 0 and c == 0, stream)
+
+    def ring_fwd_finish(self, stream=None):
+        n = self.dist_rows
+        if self.dt == torch.float32:
+            s = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(s):
+                self.o[:n].copy_(self.ring_oacc[:n])
+        else:
+            sk.skr_cast_f32_bf16(self.ring_oacc[:n], self.o[:n], stream)
+
+    def ring_bwd_start(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.ring_dq[:self.dist_rows].zero_()
+            for t in self.ring_acc(0):
+                t.zero_()
+
+    def ring_bwd_hop(self, r, vk, vv, stream=None):
+        """Hop r of the ring backward: dQ of this rank's query chunks accumulates in fp32, the visiting
+        chunks' dK / dV are added into the travelling accumulators (final O / LSE of the forward)."""
+        ak, av = self.ring_acc(r)
+        for c in (0, 1):
+            self._timed("bwd_dist", lambda c=c: sk.skr_attn_bwd_acc(
+                self.shape, self.ring_b[r][c], self.q, vk, vv, self.o, self.do, self.lse, self.ring_dq, ak, av,
+                self.ws, stream), stream)
+
+    def ring_bwd_finish(self, stream=None):
+        """After N accumulator hops this rank holds its own chunks' summed dK / dV."""
+        n = self.dist_rows
+        ak, av = self.ring_acc(self.cp)
+        if self.dt == torch.float32:
+            s = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(s):
+                self.dq[:n].copy_(self.ring_dq[:n])
+                self.dk[:n].copy_(ak[:n])
+                self.dv[:n].copy_(av[:n])
+        else:
+            sk.skr_cast_f32_bf16(self.ring_dq[:n], self.dq[:n], stream)
+            sk.skr_cast_f32_bf16(ak[:n], self.dk[:n], stream)
+            sk.skr_cast_f32_bf16(av[:n], self.dv[:n], stream)
+
+    def forward_ring(self, q_src, k_src, v_src, comm, side):
+        """Eq. 2 with the ring exchange: main packs and runs the LOCAL tiles while the side stream
+        moves the own prefix one hop; then per hop r main computes against the visiting prefix while
+        the side stream moves it on (double-buffered; a receive buffer is reused only after the hop
+        that read it)."""
+        main = torch.cuda.current_stream()
+        self.pack_qkv(q_src, k_src, v_src)
+        if not self.has_dist:
+            self.fwd_local()
+            return
+        N, P = self.cp, self.P
+        cur = (self.k[:P], self.v[:P])
+        ev_cur = torch.cuda.Event()
+        ev_cur.record(main)
+        done = [None] * N
+        recv = None
+        for r in range(N):
+            if r + 1 < N:
+                nxt = self.ring_bufs(r + 1)
+                side.wait_event(ev_cur)
+                if r >= 1:
+                    side.wait_event(done[r - 1])     # nxt was the visiting buffer of hop r - 1
+                with torch.cuda.stream(side):
+                    comm.ring_shift([cur[0], cur[1]], [nxt[0][:P], nxt[1][:P]], side)
+                    recv = torch.cuda.Event()
+                    recv.record(side)
+            if r == 0:
+                self.fwd_local()
+            self.ring_fwd_hop(r, cur[0], cur[1])
+            done[r] = torch.cuda.Event()
+            done[r].record(main)
+            if r + 1 < N:
+                main.wait_event(recv)
+                cur, ev_cur = (nxt[0][:P], nxt[1][:P]), recv
+        self.ring_fwd_finish()
+
+    def backward_ring(self, do_src, comm, side):
+        """Mirror: per hop r main computes dQ (fp32, accumulated) and the visiting chunks' dK / dV
+        (into the travelling accumulators); the side stream moves the visiting K / V on during the
+        hop and the accumulators after it; after N accumulator hops they are home. LOCAL tiles run on
+        main after the first hop's kernels."""
+        main = torch.cuda.current_stream()
+        self.pack_do(do_src)
+        if not self.has_dist:
+            self.bwd_local()
+            return
+        N, P = self.cp, self.P
+        self.ring_bwd_start()
+        cur = (self.k[:P], self.v[:P])
+        ev_cur = torch.cuda.Event()
+        ev_cur.record(main)
+        done = [None] * N
+        for r in range(N):
+            kv_recv = None
+            if r + 1 < N:
+                nxt = self.ring_bufs(r + 1)
+                side.wait_event(ev_cur)
+                if r >= 1:
+                    side.wait_event(done[r - 1])
+                with torch.cuda.stream(side):
+                    comm.ring_shift([cur[0], cur[1]], [nxt[0][:P], nxt[1][:P]], side)
+                    kv_recv = torch.cuda.Event()
+                    kv_recv.record(side)
+            self.ring_bwd_hop(r, cur[0], cur[1])
+            done[r] = torch.cuda.Event()
+            done[r].record(main)
+            # the accumulators carry this hop's contribution on to the next rank (N hops: home)
+            side.wait_event(done[r])
+            with torch.cuda.stream(side):
+                (ak, av), (bk, bv) = self.ring_acc(r), self.ring_acc(r + 1)
+                comm.ring_shift([ak[:P], av[:P]], [bk[:P], bv[:P]], side)
+                acc_recv = torch.cuda.Event()
+                acc_recv.record(side)
+            if r == 0:
+                self.bwd_local()
+            main.wait_event(acc_recv)
+            if kv_recv is not None:
+                main.wait_event(kv_recv)
+                cur, ev_cur = (nxt[0][:P], nxt[1][:P]), kv_recv
+        self.ring_bwd_finish()
 
     # ------------------------------------------------------------------ row f3: peer-memory exchange
     def connect_peer(self, peer):
@@ -469,6 +648,58 @@ def loopback_peer_fused_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
             x.bwd_dist_fused()
         for x in ranks:
             x.acc_cast()
+    for x in ranks:
+        x.bwd_local()
+    return ranks
+
+
+def loopback_ring_step(ranks, q_srcs, k_srcs, v_srcs, do_srcs):
+    """Row f4 ring CP on ONE GPU in one process: the N emulated ranks run each hop in lockstep, the
+    ring hops (point-to-point sends) replaced by device copies. Same kernels and tables as the
+    NCCL ring (RankStep.forward_ring / backward_ring)."""
+    N = len(ranks)
+    for r, x in enumerate(ranks):
+        x.pack_qkv(q_srcs[r], k_srcs[r], v_srcs[r])
+        x.pack_do(do_srcs[r])
+    for x in ranks:
+        x.fwd_local()
+    if ranks[0].has_dist:
+        P = ranks[0].P
+        vis = [(x.k[:P], x.v[:P]) for x in ranks]
+        for r in range(N):
+            for x, (vk, vv) in zip(ranks, vis):
+                x.ring_fwd_hop(r, vk, vv)
+            if r + 1 < N:   # hop: rank j receives rank j - 1's visiting prefix
+                nxt = []
+                for j, x in enumerate(ranks):
+                    bk, bv = x.ring_bufs(r + 1)
+                    bk[:P].copy_(vis[(j - 1) % N][0])
+                    bv[:P].copy_(vis[(j - 1) % N][1])
+                    nxt.append((bk[:P], bv[:P]))
+                vis = nxt
+        for x in ranks:
+            x.ring_fwd_finish()
+        for x in ranks:
+            x.ring_bwd_start()
+        vis = [(x.k[:P], x.v[:P]) for x in ranks]
+        for r in range(N):
+            for x, (vk, vv) in zip(ranks, vis):
+                x.ring_bwd_hop(r, vk, vv)
+            for j, x in enumerate(ranks):   # accumulator hop (also after the last: home)
+                bk, bv = x.ring_acc(r + 1)
+                ak, av = ranks[(j - 1) % N].ring_acc(r)
+                bk[:P].copy_(ak[:P])
+                bv[:P].copy_(av[:P])
+            if r + 1 < N:
+                nxt = []
+                for j, x in enumerate(ranks):
+                    bk, bv = x.ring_bufs(r + 1)
+                    bk[:P].copy_(vis[(j - 1) % N][0])
+                    bv[:P].copy_(vis[(j - 1) % N][1])
+                    nxt.append((bk[:P], bv[:P]))
+                vis = nxt
+        for x in ranks:
+            x.ring_bwd_finish()
     for x in ranks:
         x.bwd_local()
     return ranks

@@ -460,6 +460,44 @@ def skr_cast_f32_bf16(src, dst, stream=None):
     _check(fn(_tptr(src), _tptr(dst), src.numel(), _stream(stream)))
 
 
+# ---------------------------------------------------------------------------- row f4: ring CP
+def skr_ring_segs(mb_lens, assign, cp, rank, step, cls):
+    """Host segment tables of ring hop `step`, key-chunk class `cls` on `rank` (include/skrull.h)."""
+    L = np.ascontiguousarray(mb_lens, np.int64)
+    A = np.ascontiguousarray(assign, np.int32)
+    n = i32()
+    fn = _sig("skr_ring_segs", i32, P(i64), P(i32), i32, i32, i32, i32, i32, P(i32), P(i32), P(i32), P(i32), i32,
+              P(i32))
+    cap = 0
+    for _ in range(2):
+        cu = np.zeros(cap + 1, np.int32)
+        qp, ks, kl = (np.zeros(max(cap, 1), np.int32) for _ in range(3))
+        st = fn(_ptr(L, i64), _ptr(A, i32), len(L), int(cp), int(rank), int(step), int(cls), _ptr(cu, i32),
+                _ptr(qp, i32), _ptr(ks, i32), _ptr(kl, i32), cap, C.byref(n))
+        if st == SKR_OK:
+            m = n.value
+            return {"cu_seqlens_q": cu[:m + 1], "q_pos": qp[:m], "k_start": ks[:m], "k_len": kl[:m], "n_seg": m}
+        if st != SKR_E_CAPACITY:
+            _check(st)
+        cap = n.value
+    raise SkrullError(SKR_E_CAPACITY, "ring segments")
+
+
+def skr_attn_merge(shape, o_part, lse_part, o_acc, lse_acc, row_begin, row_end, first, stream=None):
+    fn = _sig("skr_attn_merge", i32, P(skr_attn_shape), vp, vp, vp, vp, i32, i32, i32, i32, vp)
+    _check(fn(C.byref(shape), _tptr(o_part), _tptr(lse_part), _tptr(o_acc), _tptr(lse_acc), int(row_begin),
+              int(row_end), lse_acc.shape[-1], int(first), _stream(stream)))
+
+
+def skr_attn_bwd_acc(shape, segs: DeviceSegs, q, k, v, o, dout, lse, dq, dk, dv, ws, stream=None):
+    fn = _sig("skr_attn_bwd_acc", i32, P(skr_attn_shape), P(skr_segs), vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32,
+              vp, C.c_size_t, vp)
+    g = segs.struct()
+    _check(fn(C.byref(shape), C.byref(g), _tptr(q), _tptr(k), _tptr(v), _tptr(o), _tptr(dout), _tptr(lse), _tptr(dq),
+              _tptr(dk), _tptr(dv), q.shape[0], k.shape[0], _tptr(ws), ws.numel() * ws.element_size(),
+              _stream(stream)))
+
+
 # ---------------------------------------------------------------------------- a5-a9 composite step
 class skr_cp_step(C.Structure):
     _fields_ = [("local_fwd", skr_segs), ("local_bwd", skr_segs), ("dist_fwd", skr_segs), ("dist_bwd", skr_segs),
@@ -636,6 +674,15 @@ class Comm:
     def all_reduce_f32(self, buf, stream=None):
         _check(_sig("skr_comm_all_reduce_f32", i32, vp, vp, C.c_size_t, vp)(
             self.h, _tptr(buf), buf.numel(), _stream(stream)))
+
+    def ring_shift(self, sends, recvs, stream=None):
+        """One ring hop (row f4): sends[i] to rank + 1, rank - 1's into recvs[i] (one NCCL group)."""
+        n = len(sends)
+        sb = (vp * max(n, 1))(*[_tptr(t) for t in sends])
+        rb = (vp * max(n, 1))(*[_tptr(t) for t in recvs])
+        nb = (C.c_size_t * max(n, 1))(*[t.numel() * t.element_size() for t in sends])
+        _check(_sig("skr_comm_ring_shift", i32, vp, vp, vp, vp, i32, vp)(
+            self.h, C.cast(sb, vp), C.cast(rb, vp), C.cast(nb, vp), n, _stream(stream)))
 
     def size(self):
         """-> (nranks, rank) as the library sees the communicator."""

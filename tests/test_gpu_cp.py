@@ -43,7 +43,7 @@ def _baseline_plan(sk, lens, C, N, planner):
 def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1, exchange="nccl", planner="skrull"):
     from paper_2505_19609_b200 import skrull as sk
     from paper_2505_19609_b200.runtime import (RankStep, dp_micro_batches, gather_rank_natural, loopback_peer_fused_step,
-                                               loopback_peer_step, loopback_step)
+                                               loopback_peer_step, loopback_ring_step, loopback_step)
     shape = sk.attn_shape(hq, hkv, d, sk.SKR_BF16 if bf16 else sk.SKR_FP32)
     if planner == "skrull":
         p = sk.skr_plan(lens, C, N, dp, hq * d, hkv * d)
@@ -65,10 +65,11 @@ def _run(lens, hq, hkv, d, N, C, bf16, seed, dp=1, exchange="nccl", planner="skr
     for idx, ml, ma in [mb for dr in range(dp) for mb in dp_micro_batches(p, lens, dr)]:
         n_dist += int((ma == -1).sum())
         mb_inputs = [inputs[i] for i in idx]
-        ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
+        ranks = [RankStep(shape, ml, ma, N, r, ring=exchange == "ring") for r in range(N)]
         srcs = {k: [torch.from_numpy(gather_rank_natural(mb_inputs, ml, ma, N, r, k)).to("cuda", tdt)
                     for r in range(N)] for k in ("q", "k", "v", "do")}
-        step = {"peer": loopback_peer_step, "fused": loopback_peer_fused_step}.get(exchange, loopback_step)
+        step = {"peer": loopback_peer_step, "fused": loopback_peer_fused_step,
+                "ring": loopback_ring_step}.get(exchange, loopback_step)
         step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
         torch.cuda.synchronize()
         for r, rs in enumerate(ranks):
@@ -134,12 +135,13 @@ def test_dp2_x_cp2_grid():
     assert set(p["dp_of_seq"]) == {0, 1} and n_dist >= 1
 
 
-@pytest.mark.parametrize("exchange", ["peer", "fused"])
+@pytest.mark.parametrize("exchange", ["peer", "fused", "ring"])
 @pytest.mark.parametrize("case", ["c1_fp32", "bf16_n2", "bf16_n4", "rollback_d64"])
 def test_peer_exchange_loopback(case, exchange):
     # row f3: the a6 / a9 exchange as peer-gather / peer-reduce kernels (one pass each, "peer") or
     # with the a9 reduction fused into the distributed backward kernel's epilogue ("fused", step
-    # two) instead of all-gather + reorder and permute + reduce-scatter + cast; same oracle bar
+    # two) instead of all-gather + reorder and permute + reduce-scatter + cast; row f4: ring CP
+    # ("ring": K/V hops, partial attentions merged, travelling dK/dV accumulators); same oracle bar
     lens = [1500, 37, 300, 129, 1, 600, 64, 2000, 250]
     if case == "c1_fp32":
         n_dist, _ = _run([17, 33, 64, 90, 128, 200, 256, 300], 2, 2, 64, 2, 600, False, 0, exchange=exchange)
@@ -209,10 +211,10 @@ def test_random_plans_fuzz(case):
     lens = [int(min(3000, max(1, rng.lognormvariate(5.0, 1.4)))) for _ in range(K)]
     lo = max(max(lens) // N + 1, 64)
     C = rng.randint(lo, max(lo, sum(lens) // N + 256))
-    # every 6th case in fp32 test mode; every 3rd through the row-f3 peer-memory exchange (step one),
-    # every 3rd through its fused step two
+    # every 6th case in fp32 test mode; a quarter of the cases through each exchange: all-gather /
+    # reduce-scatter, the row-f3 peer-memory exchange (step one), its fused step two, the row-f4 ring
     _run(lens, hq, hkv, d, N, C, case % 6 != 5, 50 + case,
-         exchange={0: "nccl", 1: "peer", 2: "fused"}[case % 3])
+         exchange={0: "nccl", 1: "peer", 2: "fused", 3: "ring"}[case % 4])
 
 
 @pytest.mark.parametrize("planner", ["rr", "rr_norb", "full_shard"])

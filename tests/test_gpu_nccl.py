@@ -26,9 +26,10 @@ from tests.attn_harness import make_inputs, tol_ok  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run_nccl_step(lens, assign, hq, hkv, d, bf16, seed, cp=1, rank=0, comm=None, reps=1):
+def run_nccl_step(lens, assign, hq, hkv, d, bf16, seed, cp=1, rank=0, comm=None, reps=1, ring=False):
     """One micro-batch on CP rank `rank` through skr_cp_attn_fwd / _bwd with `comm` (a 1-rank
-    communicator when None). Returns the per-sequence outputs this rank owns:
+    communicator when None), or with ring=True through the row-f4 ring CP (forward_ring /
+    backward_ring: NCCL point-to-point hops). Returns the per-sequence outputs this rank owns:
     {seq: {key: (q_lo, array)}} plus the RankStep."""
     from paper_2505_19609_b200 import skrull as sk
     from paper_2505_19609_b200.runtime import RankStep, gather_rank_natural
@@ -39,13 +40,17 @@ def run_nccl_step(lens, assign, hq, hkv, d, bf16, seed, cp=1, rank=0, comm=None,
     if own:
         comm = sk.Comm(1, 0)
     assert comm.size() == (cp, rank)
-    rs = RankStep(shape, np.asarray(lens), np.asarray(assign, np.int32), cp, rank)
+    rs = RankStep(shape, np.asarray(lens), np.asarray(assign, np.int32), cp, rank, ring=ring)
     src = {k: torch.from_numpy(gather_rank_natural(inputs, lens, assign, cp, rank, k)).to("cuda", tdt)
            for k in ("q", "k", "v", "do")}
     side = torch.cuda.Stream(priority=-1)
     for _ in range(reps):      # repeated steps reuse every buffer (the bench's steady state)
-        rs.forward(src["q"], src["k"], src["v"], comm, side)
-        rs.backward(src["do"], comm, side)
+        if ring:
+            rs.forward_ring(src["q"], src["k"], src["v"], comm, side)
+            rs.backward_ring(src["do"], comm, side)
+        else:
+            rs.forward(src["q"], src["k"], src["v"], comm, side)
+            rs.backward(src["do"], comm, side)
     comm.wait(torch.cuda.current_stream(), timeout_s=120.0)     # polls ncclCommGetAsyncError
     comm.check()
     torch.cuda.synchronize()
@@ -101,6 +106,17 @@ def test_nccl_exchange_one_rank(case):
     check_against_oracle(inputs, [out], lens, bf16)
 
 
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_nccl_ring_one_rank(case):
+    # row f4's ring CP on a 1-rank communicator: the hop-0 partial attentions (diagonal and full
+    # chunk pairs, the merge) and the travelling dK/dV accumulators' hop through ncclSend / ncclRecv
+    # to itself; two steps (buffer reuse)
+    lens, assign, hq, hkv, d, bf16 = CASES[case]
+    inputs, out, rs = run_nccl_step(lens, assign, hq, hkv, d, bf16, seed=33, reps=2, ring=True)
+    assert rs.ring
+    check_against_oracle(inputs, [out], lens, bf16)
+
+
 def test_comm_rank_count_mismatch_is_rejected():
     # a step planned for CP = 2 must not run on a 1-rank communicator (ADVICE: cp_step.cu nranks check)
     from paper_2505_19609_b200 import skrull as sk
@@ -133,21 +149,23 @@ torch.cuda.set_device(rank)
 dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
 comm = sk.Comm(2, rank, group=dist.group.WORLD, src=0)
 lens, assign, hq, hkv, d, bf16 = CASES[os.environ["CASE"]]
-inputs, out, rs = run_nccl_step(lens, assign, hq, hkv, d, bf16, seed=31, cp=2, rank=rank, comm=comm, reps=2)
+inputs, out, rs = run_nccl_step(lens, assign, hq, hkv, d, bf16, seed=31, cp=2, rank=rank, comm=comm, reps=2,
+                                ring=os.environ.get("RING") == "1")
 np.save(os.path.join(os.environ["OUT"], f"r{rank}.npy"), np.array([out], dtype=object), allow_pickle=True)
 comm.close()
 dist.destroy_process_group()
 '''
 
 
+@pytest.mark.parametrize("ring", [False, True])
 @pytest.mark.parametrize("case", ["bf16_d128", "fp32_toy_c1"])
-def test_nccl_exchange_two_ranks(case, tmp_path):
+def test_nccl_exchange_two_ranks(case, ring, tmp_path):
     # the same hand-assigned step over a real 2-rank NCCL communicator (2 GPUs), both ranks' outputs
     # together against the oracle; skipped on a 1-GPU box
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     env = dict(os.environ, ROOT=ROOT, CASE=case, OUT=str(tmp_path), MASTER_ADDR="127.0.0.1", MASTER_PORT="29561",
-               WORLD_SIZE="2")
+               WORLD_SIZE="2", RING="1" if ring else "0")
     procs = [subprocess.Popen([sys.executable, "-c", _TWO_RANK], env=dict(env, RANK=str(r), LOCAL_RANK=str(r)),
                               cwd=ROOT) for r in range(2)]
     for p in procs:

@@ -313,3 +313,44 @@ def test_header_is_plain_c_and_links(tmp_path):
                     "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
     assert int(out[0]) == skrull.skr_abi_version() and int(out[1]) == 15204352
+
+
+def test_ring_segments_visit_every_causal_key_chunk_once():
+    # row f4 (ring CP): over the N hops and both key-chunk classes, every own query chunk c of every
+    # distributed sequence sees each non-empty key chunk c' <= c exactly once -- whole when c' < c
+    # (q_pos = its length), the causal diagonal when c' == c -- at the rows that chunk occupies in
+    # the visiting rank's packed prefix (skr_pack_chunks), and nothing after c
+    rng = random.Random(18)
+    for it in range(120):
+        N = rng.randint(1, 5)
+        K = rng.randint(1, 7)
+        lens = [rng.choice([1, 2, 3, 7, 64, 129, 300, 1000]) for _ in range(K)]
+        assign = [-1 if rng.random() < 0.5 else rng.randrange(N) for _ in range(K)]
+        table = skrull.skr_pack_chunks(lens, assign, N)
+        P = skrull.skr_pack_bounds(lens, assign, N, 0)["pad_rows_P"]
+        where = {(int(t[0]), int(t[1])): (int(t[3]) - int(t[2]) * P, int(t[5])) for t in table}
+        dist = [k for k in sorted(range(K), key=lambda k: (lens[k], k)) if assign[k] == -1]
+        for j in range(N):
+            pr = skrull.skr_pack_rank(lens, assign, N, j)
+            nd = 2 * len(dist)
+            seen = {}
+            for r in range(N):
+                s = (j - r) % N
+                for cls in (0, 1):
+                    t = skrull.skr_ring_segs(lens, assign, N, j, r, cls)
+                    assert t["n_seg"] == nd
+                    assert list(t["cu_seqlens_q"]) == list(pr["cu_seqlens_q"][:nd + 1])
+                    ck = s if cls == 0 else 2 * N - 1 - s
+                    for i in range(nd):
+                        k, c = dist[i // 2], (j, 2 * N - 1 - j)[i % 2]
+                        if t["k_len"][i] == 0:
+                            assert ck > c or where[(k, ck)][1] == 0
+                            continue
+                        off, ln = where[(k, ck)]
+                        assert ck <= c and t["k_start"][i] == off and t["k_len"][i] == ln
+                        assert t["q_pos"][i] == (ln if ck < c else 0)
+                        assert (k, c, ck) not in seen
+                        seen[(k, c, ck)] = 1
+            want = {(k, c, cc) for k in dist for c in (j, 2 * N - 1 - j) for cc in range(c + 1)
+                    if where[(k, cc)][1] > 0}
+            assert set(seen) == want
