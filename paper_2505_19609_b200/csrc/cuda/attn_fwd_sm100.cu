@@ -156,6 +156,16 @@ constexpr int kSplitP = 6;
 // their row maxima through shared memory (576 threads, <= 112 registers). 1 (d = 128 only): one
 // warpgroup per head, thread = one full row of S (no cross-warpgroup exchange), P handed to the MMA in
 // two parts (kSplitP) -- 320 threads, <= 200 registers.
+// Softmax layout of the two-warpgroup-per-head kernel: 1 = row split (each warp owns 16 rows and all
+// key columns, TMEM 16x256b loads, max / sum combined with shuffles); 0 = column split (each
+// warpgroup owns half the key columns of all 128 rows, maxima exchanged through shared memory).
+// Row split measured -4 to -6 % cycles at d = 128 (S4n1, C5n1) and -12 % at d = 64 (C2)
+// (profiles/r02_experiments.md); the column split is kept as the documented alternative.
+#ifndef SKR_FWD_ROWSPLIT
+#define SKR_FWD_ROWSPLIT 1
+#endif
+constexpr bool kRowSplit = SKR_FWD_ROWSPLIT;
+
 template <int D, int kPolyPer8, int kWG = 2>
 __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -604,6 +614,155 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         }
       }
       if (store) lse[(size_t)h * a.ld_lse + r0 + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+    }
+  } else if constexpr (kRowSplit) {
+    // ================= softmax, row split: head s = warp / 8; each of the head's 8 warps owns 16 query
+    // rows (TMEM lanes 32 (warp % 4) + 16 ((warp / 4) % 2) + [0, 16)) and all BN key columns, read
+    // with the 16x256b shape: thread t holds rows t/4 and t/4 + 8 of its 16, 32 key columns of each;
+    // the four threads of a row combine its max (per tile) and sum (once) with two shuffles -- no
+    // shared-memory exchange and no barrier between warps (the two-warpgroup column split needs both)
+    const int s = warp / 8, hr = (warp / 4) % 2;
+    const int h = s == 0 ? ha : hb;
+    if (h >= 0) {
+      const int lane0 = 32 * (warp % 4) + 16 * hr;            // this warp's first TMEM lane (= tile row)
+      const uint32_t lane_base = (uint32_t)lane0 << 16;
+      const uint32_t tS = tmem + lane_base + C::tS(s);
+      const uint32_t tO = tmem + lane_base + C::tO(s);
+      const uint32_t tP = tmem + lane_base + C::tP(s);
+      const int rA = lane0 + lane / 4, rB = rA + 8;            // tile rows of this thread
+      const int qA = qp0 + rA, qB = qp0 + rB;                  // their query positions
+      const int cq = 2 * (lane % 4);                           // this thread's 2 columns of each group of 8
+      const float sl2 = a.scale * 1.4426950408889634f;
+      float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;   // l: this thread's partial row sums
+      for (int j = 0; j < n_kv; ++j) {
+        mbar_wait(&bars->s_full[s], j & 1);
+        tc_fence_after();
+        float x[BN / 2];
+        {
+          uint32_t r[BN / 2];
+          tmem_ld16x256_x16(tS, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < BN / 2; ++i) x[i] = __uint_as_float(r[i]);
+        }
+        if (!C::kPAlias) {
+          tc_fence_before();
+          mbar_arrive(&bars->s_free[s]);      // S_s TMEM may now take S_s(j+1)
+        }
+        const int kv0 = j * BN;
+        if (kv0 + BN - 1 > qp0 || kv0 + BN > k_len) {   // diagonal / last tile: mask keys after the query
+#pragma unroll
+          for (int k = 0; k < BN / 8; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int key = kv0 + 8 * k + cq + e;
+              if (key > qA || key >= k_len) x[4 * k + e] = -INFINITY;
+              if (key > qB || key >= k_len) x[4 * k + 2 + e] = -INFINITY;
+            }
+        }
+        // row maxima: 4 independent fmax3 chains per row over this thread's 32 columns, then the row's
+        // four threads (lanes 4i..4i+3) combine with two xor shuffles
+        float ma[4], mb[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) ma[t] = x[4 * t], mb[t] = x[4 * t + 2];
+#pragma unroll
+        for (int k = 0; k < BN / 8; k += 4)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            ma[t] = fmax3(ma[t], x[4 * (k + t) + 1], k + 4 < BN / 8 ? x[4 * (k + 4 + t)] : x[4 * (k + t) + 1]);
+            mb[t] = fmax3(mb[t], x[4 * (k + t) + 3], k + 4 < BN / 8 ? x[4 * (k + 4 + t) + 2] : x[4 * (k + t) + 3]);
+          }
+        float mxA = fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3]));
+        float mxB = fmaxf(fmaxf(mb[0], mb[1]), fmaxf(mb[2], mb[3]));
+        mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 1));
+        mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 1));
+        mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 2));
+        mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 2));
+        const float nA = fmaxf(mA, mxA * sl2), nB = fmaxf(mB, mxB * sl2);
+        // tcgen05.ld/st are warp-collective: the lazy-rescale decision is made per warp (its 16 rows)
+        const bool rescale =
+            __any_sync(0xffffffffu, nA > mA + kRescaleThreshold || nB > mB + kRescaleThreshold) || j == 0;
+        const float alA = (rescale && j > 0) ? ex2(mA - nA) : 1.f, alB = (rescale && j > 0) ? ex2(mB - nB) : 1.f;
+        if (rescale) mA = nA, mB = nB;
+        const float2 sl2_2 = make_float2(sl2, sl2);
+        const float2 negA = make_float2(mA == -INFINITY ? 0.f : -mA, mA == -INFINITY ? 0.f : -mA);
+        const float2 negB = make_float2(mB == -INFINITY ? 0.f : -mB, mB == -INFINITY ? 0.f : -mB);
+        float2 sA = make_float2(0.f, 0.f), sB = make_float2(0.f, 0.f);
+        uint32_t pk[BN / 4];
+#pragma unroll
+        for (int k = 0; k < BN / 8; ++k) {
+          const float2 ea = ffma2(make_float2(x[4 * k], x[4 * k + 1]), sl2_2, negA);
+          const float2 eb = ffma2(make_float2(x[4 * k + 2], x[4 * k + 3]), sl2_2, negB);
+          // kPolyPer8 of every 8 exponentials on the FMA pipe (element index 4k + e within the thread)
+          const int b = (4 * k) % 8;
+          const float pa0 = b + 0 < kPolyPer8 ? ex2_poly(ea.x) : ex2(ea.x);
+          const float pa1 = b + 1 < kPolyPer8 ? ex2_poly(ea.y) : ex2(ea.y);
+          const float pb0 = b + 2 < kPolyPer8 ? ex2_poly(eb.x) : ex2(eb.x);
+          const float pb1 = b + 3 < kPolyPer8 ? ex2_poly(eb.y) : ex2(eb.y);
+          sA = fadd2(sA, make_float2(pa0, pa1));
+          sB = fadd2(sB, make_float2(pb0, pb1));
+          pk[2 * k] = pack_bf16(pa0, pa1);
+          pk[2 * k + 1] = pack_bf16(pb0, pb1);
+        }
+        // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
+        if (j > 0) {
+          mbar_wait(&bars->pv_done[s], (j - 1) & 1);
+          tc_fence_after();
+        }
+        if (rescale && j > 0) {
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {               // 32 columns (16 registers) at a time
+            uint32_t o[16];
+            tmem_ld16x256_x4(tO + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 va = fmul2(make_float2(__uint_as_float(o[4 * k]), __uint_as_float(o[4 * k + 1])),
+                                      make_float2(alA, alA));
+              const float2 vb = fmul2(make_float2(__uint_as_float(o[4 * k + 2]), __uint_as_float(o[4 * k + 3])),
+                                      make_float2(alB, alB));
+              o[4 * k] = __float_as_uint(va.x), o[4 * k + 1] = __float_as_uint(va.y);
+              o[4 * k + 2] = __float_as_uint(vb.x), o[4 * k + 3] = __float_as_uint(vb.y);
+            }
+            tmem_st16x256_x4(tO + c, o);
+          }
+        }
+        lA = (rescale ? (j == 0 ? 0.f : lA * alA) : lA) + (sA.x + sA.y);
+        lB = (rescale ? (j == 0 ? 0.f : lB * alB) : lB) + (sB.x + sB.y);
+        tmem_st16x128_x16(tP, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full[s]);
+      }
+      // ---- epilogue: the row sums of the four threads of a row, O / l -> bf16, LSE
+      lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+      lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+      lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+      lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+      mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
+      tc_fence_after();
+      const float iA = 1.f / lA, iB = 1.f / lB;
+      __nv_bfloat16* oA = out + ((size_t)(r0 + rA) * a.hq + h) * D + cq;
+      __nv_bfloat16* oB = out + ((size_t)(r0 + rB) * a.hq + h) * D + cq;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {                    // 32 columns (16 registers) at a time
+        uint32_t o[16];
+        tmem_ld16x256_x4(tO + c, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (rA < n_valid)
+            *reinterpret_cast<uint32_t*>(oA + c + 8 * k) =
+                pack_bf16(__uint_as_float(o[4 * k]) * iA, __uint_as_float(o[4 * k + 1]) * iA);
+          if (rB < n_valid)
+            *reinterpret_cast<uint32_t*>(oB + c + 8 * k) =
+                pack_bf16(__uint_as_float(o[4 * k + 2]) * iB, __uint_as_float(o[4 * k + 3]) * iB);
+        }
+      }
+      if (lane % 4 == 0) {
+        if (rA < n_valid) lse[(size_t)h * a.ld_lse + r0 + rA] = (mA + __log2f(lA)) * 0.6931471805599453f;
+        if (rB < n_valid) lse[(size_t)h * a.ld_lse + r0 + rB] = (mB + __log2f(lB)) * 0.6931471805599453f;
+      }
     }
   } else {
     // ================= softmax: head s = warp / 8, key-column half hf = (warp / 4) % 2
