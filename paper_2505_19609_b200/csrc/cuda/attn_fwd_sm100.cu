@@ -273,7 +273,9 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
     pa.mark(1);
     if (lane == 0) pa.flush(g_trace_smem, kTmaW);
   } else if (warp == kMmaW) {
-    // ================= MMA issuer: ONE elected thread runs the whole loop. Measured (profiles/
+    // ================= MMA issuer: ONE elected thread runs the whole loop. Its waits spin on plain
+    // try_wait (the suspend-hinted form measured 1.5 % slower here and 3 % faster in the backward,
+    // profiles/r02_experiments.md). Measured (profiles/
     // umma_probe.py): the tensor pipe buffers only about one MMA ahead of the issuing thread, and
     // re-entering an elected region per MMA group costs ~200 cycles (R2UR of the descriptors,
     // BSSY/ELECT); inside a single elect.sync region groups + commits stream at the MMA floor.
@@ -304,12 +306,12 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
       // kWG = 1: PV in two parts, each waiting for its share of P (split hand-over)
       auto issue_pv_split = [&](int s, int u, bool acc, int jv) {
         const uint64_t dv = dv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
-        mbar_wait_sleep(&bars->p_lo[s], jv & 1);
+        mbar_wait(&bars->p_lo[s], jv & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kSplitP; ++k)
           umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
-        mbar_wait_sleep(&bars->p_full[s], jv & 1);
+        mbar_wait(&bars->p_full[s], jv & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = kSplitP; k < BN / 16; ++k)
@@ -336,13 +338,13 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
       auto wait_k = [&](int j) {
         pa.mark(3);
         for (int t = 0; t < nstream; ++t)
-          mbar_wait_sleep(&bars->kv_full[kunit(j, t)], (kidx(j, t) / C::kUnits) & 1);
+          mbar_wait(&bars->kv_full[kunit(j, t)], (kidx(j, t) / C::kUnits) & 1);
         pa.mark(0);
       };
       auto wait_v = [&](int j) {
         pa.mark(3);
         for (int t = 0; t < nstream; ++t)
-          mbar_wait_sleep(&bars->kv_full[vunit(j, t)], (vidx(j, t) / C::kUnits) & 1);
+          mbar_wait(&bars->kv_full[vunit(j, t)], (vidx(j, t) / C::kUnits) & 1);
         pa.mark(1);
       };
       auto free_k = [&](int j) {
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
             wait_k(j);
             for (int s = 0; s < nq; ++s) {
               pa.mark(3);
-              if (j > 0) mbar_wait_sleep(&bars->s_free[s], (j - 1) & 1);
+              if (j > 0) mbar_wait(&bars->s_free[s], (j - 1) & 1);
               pa.mark(2);
               tc_fence_after();
               trace(5 + s, j);
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
               pa.mark(3);
               trace(7 + s, jv);
               if (kWG == 2) {
-                mbar_wait_sleep(&bars->p_full[s], jv & 1);
+                mbar_wait(&bars->p_full[s], jv & 1);
                 pa.mark(2);
                 tc_fence_after();
                 issue_pv(s, vunit(jv, s), jv > 0);
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
           for (int s = 0; s < nq; ++s) {
             pa.mark(3);
             if (kWG == 2) {
-              mbar_wait_sleep(&bars->p_full[s], jv & 1);
+              mbar_wait(&bars->p_full[s], jv & 1);
               pa.mark(2);
               tc_fence_after();
               trace(7 + s, jv);
@@ -704,8 +706,10 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
           pk[2 * k] = pack_bf16(pa0, pa1);
           pk[2 * k + 1] = pack_bf16(pb0, pb1);
         }
-        // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched
-        if (j > 0) {
+        // PV_s(j-1) must have read P_s(j-1) and finished accumulating O_s before P / O are touched.
+        // With P aliasing S (d = 128) that is implied by s_full(j): S_s(j) was issued after PV_s(j-1)
+        // and the tensor pipe completes in order, so the wait (and its fence) is skipped.
+        if (!C::kPAlias && j > 0) {
           mbar_wait(&bars->pv_done[s], (j - 1) & 1);
           tc_fence_after();
         }
