@@ -1,7 +1,7 @@
 """compute-sanitizer target: toy C1 (BASELINE configs[0]) at CP = 2 through the CP
 runtime with the loopback exchange, in bf16 (tcgen05 kernels) and in fp32 test mode, plus the
 composite skr_cp_attn_fwd / _bwd step on a 1-rank NCCL communicator with hand-distributed
-sequences, and the query-banded backward work lists (band_rows = 128). Small on purpose: every launch runs under the sanitizer's instrumentation.
+sequences, the query-banded backward work lists (band_rows = 128) and the ring-CP exchange. Small on purpose: every launch runs under the sanitizer's instrumentation.
 
     compute-sanitizer --tool memcheck python profiles/sanitize_c1.py
 """
@@ -13,21 +13,22 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_19609_b200 import skrull as sk  # noqa: E402
-from paper_2505_19609_b200.runtime import RankStep, gather_rank_natural, loopback_step  # noqa: E402
+from paper_2505_19609_b200.runtime import (RankStep, gather_rank_natural, loopback_ring_step,  # noqa: E402
+                                           loopback_step)
 from synth import seq_tensors  # noqa: E402
 
 LENS = [17, 33, 64, 90, 128, 200, 256, 300]
 
 
-def run(dtype, hq, hkv, d, N=2, C=600, band=None):
+def run(dtype, hq, hkv, d, N=2, C=600, band=None, ring=False):
     shape = sk.attn_shape(hq, hkv, d, dtype)
     p = sk.skr_plan(LENS, C, N, 1, hq * d, hkv * d)
     tdt = torch.bfloat16 if dtype == sk.SKR_BF16 else torch.float32
     inputs = [seq_tensors(0, i, S, hq, hkv, d, bf16=dtype == sk.SKR_BF16) for i, S in enumerate(LENS)]
-    ranks = [RankStep(shape, np.asarray(LENS), p["assign"], N, r, band_rows=band) for r in range(N)]
+    ranks = [RankStep(shape, np.asarray(LENS), p["assign"], N, r, band_rows=band, ring=ring) for r in range(N)]
     srcs = {k: [torch.from_numpy(gather_rank_natural(inputs, LENS, p["assign"], N, r, k)).to("cuda", tdt)
                 for r in range(N)] for k in ("q", "k", "v", "do")}
-    loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+    (loopback_ring_step if ring else loopback_step)(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
     torch.cuda.synchronize()
     return ranks
 
@@ -54,5 +55,7 @@ if __name__ == "__main__":
     run(sk.SKR_FP32, 2, 2, 64)
     run(sk.SKR_BF16, 4, 2, 128, band=128)   # query-banded backward items (band accumulators, zero / cast)
     run(sk.SKR_FP32, 2, 2, 64, band=128)
+    run(sk.SKR_BF16, 4, 2, 128, ring=True)   # row f4's ring CP (partials, merge, accumulate-mode backward)
+    run(sk.SKR_FP32, 2, 2, 64, ring=True)
     run_nccl()
     print("sanitize target done")
