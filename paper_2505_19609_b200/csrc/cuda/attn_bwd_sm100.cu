@@ -57,10 +57,13 @@ constexpr int BN = 128;  // key tile
 // group's Q / dO / dQ rows. d = 128 uses 1 (S4n1 bwd DRAM 166 -> 120 GB per launch, C5n1 bwd
 // -5 %); d = 64 keeps 0 (profiles/r02_experiments.md).
 constexpr int kThreads = 448;
-// scale * P folded into the exponent (see the producer warp): S4n1 backward -9 % instructions,
-// +0.3 % S4n1 (profiles/r02_experiments.md); 0 restores the unfolded arithmetic
+// scale * P folded into the exponent (see the producer warp): S4n1 backward -9 % instructions but
+// only +0.3 % S4n1, and LESS accurate -- scale (1/sqrt(d), not a power of two) moves the large P
+// values into the coarse start of their bf16 binade (P ~ 1 -> 0.088: relative ulp 2^-7.5 instead of
+// 2^-8), which doubled the share of dV elements above 2e-2 and failed the C3n2 full-size parity
+// (profiles/r02_experiments.md). Off: the exact arithmetic is the default.
 #ifndef SKR_BWD_SCALE_FOLD
-#define SKR_BWD_SCALE_FOLD 1
+#define SKR_BWD_SCALE_FOLD 0
 #endif
 constexpr bool kFold = SKR_BWD_SCALE_FOLD;
 constexpr int kComputeThreads = 256;

@@ -296,12 +296,16 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         }
         umma_commit(&bars->s_full[s]);
       };
-      auto issue_pv = [&](int s, int u, bool acc) {
+      // Row split with P aliasing S: the softmax never waits for an intermediate PV (s_full(j) implies
+      // PV(j-1)), so pv_done is committed once, after the last PV (an arrive nobody waits for is what
+      // compute-sanitizer's synccheck reports); its epilogue waits for phase 0
+      constexpr bool kLastPvOnly = C::kPAlias && kRowSplit && kWG == 2;
+      auto issue_pv = [&](int s, int u, bool acc, bool last = true) {
         const uint64_t dv = dv0 + ((uint32_t)(u * C::kKVBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
           umma_f16_ts(tmem + C::tO(s), tmem + C::tP(s) + k * 8, dv + ((uint32_t)(k * 2048) >> 4), id_o, acc || k > 0);
-        umma_commit(&bars->pv_done[s]);
+        if (!kLastPvOnly || last) umma_commit(&bars->pv_done[s]);
       };
       // kWG = 1: PV in two parts, each waiting for its share of P (split hand-over)
       auto issue_pv_split = [&](int s, int u, bool acc, int jv) {
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
               pa.mark(2);
               tc_fence_after();
               trace(7 + s, jv);
-              issue_pv(s, vunit(jv, s), jv > 0);
+              issue_pv(s, vunit(jv, s), jv > 0, j == n_kv);
             } else {
               trace(7 + s, jv);
               issue_pv_split(s, vunit(jv, s), jv > 0, jv);
@@ -743,7 +747,7 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
       lB += __shfl_xor_sync(0xffffffffu, lB, 1);
       lA += __shfl_xor_sync(0xffffffffu, lA, 2);
       lB += __shfl_xor_sync(0xffffffffu, lB, 2);
-      mbar_wait(&bars->pv_done[s], (n_kv - 1) & 1);
+      mbar_wait(&bars->pv_done[s], C::kPAlias ? 0 : (n_kv - 1) & 1);   // kPAlias: one commit (the last PV)
       tc_fence_after();
       const float iA = 1.f / lA, iB = 1.f / lB;
       __nv_bfloat16* oA = out + ((size_t)(r0 + rA) * a.hq + h) * D + cq;
