@@ -114,6 +114,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define SKR_FWD_BN128 128   // key-tile width of the d = 128 forward (64: separate P columns, see Cfg)
 #endif
 
+#ifndef SKR_FWD_ROWSPLIT
+#define SKR_FWD_ROWSPLIT 1
+#endif
+#ifndef SKR_FWD_PVFIRST
+#define SKR_FWD_PVFIRST 0
+#endif
+
 template <int D>
 struct Cfg {
   static constexpr int BN = D == 128 ? SKR_FWD_BN128 : 128;   // keys per K/V tile
@@ -123,11 +130,15 @@ struct Cfg {
 #ifndef SKR_FWD_UNITS64
 #define SKR_FWD_UNITS64 6
 #endif
-  static constexpr int kUnits = D == 128 ? (BN == 64 ? 8 : 4) : SKR_FWD_UNITS64;   // K/V ring depth (tiles), <= 8
+#ifndef SKR_FWD_UNITS128
+#define SKR_FWD_UNITS128 4
+#endif
+  static constexpr int kUnits = D == 128 ? (BN == 64 ? 8 : SKR_FWD_UNITS128) : SKR_FWD_UNITS64;   // K/V ring depth (tiles), <= 8
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQBytes;
   static constexpr int kOffRed = kOffKV + kUnits * kKVBytes;   // [head][tile parity][half][row] row maxima
-  static constexpr int kOffBar = kOffRed + 2 * 2 * 2 * BM * 4;
+  // (the row-split softmax exchanges nothing through shared memory: no reduction buffer)
+  static constexpr int kOffBar = kOffRed + (SKR_FWD_ROWSPLIT ? 0 : 2 * 2 * 2 * BM * 4);
   static constexpr int kSmem = kOffBar + 256 + 1024;    // + barriers + alignment slack
   // TMEM columns. P (bf16 pairs) is the A operand of O += P V straight from TMEM (no smem traffic).
   // d = 64 : S_A[0,128) S_B[128,256) O_A[256,320) O_B[320,384) P_A[384,448) P_B[448,512)
@@ -161,9 +172,7 @@ constexpr int kSplitP = 6;
 // warpgroup owns half the key columns of all 128 rows, maxima exchanged through shared memory).
 // Row split measured -4 to -6 % cycles at d = 128 (S4n1, C5n1) and -12 % at d = 64 (C2)
 // (profiles/r02_experiments.md); the column split is kept as the documented alternative.
-#ifndef SKR_FWD_ROWSPLIT
-#define SKR_FWD_ROWSPLIT 1
-#endif
+
 constexpr bool kRowSplit = SKR_FWD_ROWSPLIT;
 
 template <int D, int kPolyPer8, int kWG = 2>
@@ -400,7 +409,9 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         for (int j = 1; j <= n_kv; ++j) {
           const int jv = j - 1;
           wait_v(jv);
+#if !SKR_FWD_PVFIRST
           if (j < n_kv) wait_k(j);
+#endif
           for (int s = 0; s < nq; ++s) {
             pa.mark(3);
             if (kWG == 2) {
@@ -414,6 +425,9 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
               issue_pv_split(s, vunit(jv, s), jv > 0, jv);
               pa.mark(2);
             }
+#if SKR_FWD_PVFIRST
+            if (s == 0 && j < n_kv) wait_k(j);   // PV_A(j-1) needs only V(j-1): issue it before K(j) lands
+#endif
             if (j < n_kv) issue_s(s, kunit(j, s));
             trace(3 + s, jv);
           }

@@ -1,10 +1,12 @@
 """Test harness: build packed varlen inputs from per-sequence synthetic tensors, run the CUDA path
 through the C-ABI binding, and compare with the fp64 oracle sequence by sequence.
 
-Tolerances (BASELINE.json north_star; readings R34 / R34'):
+Tolerances (BASELINE.json north_star; readings R34 / R34' / R34''):
   bf16: |gpu - oracle| <= 2e-2 + halfulp_bf16(max(|oracle|, |gpu|)) elementwise, per tensor
         (O, dQ, dK, dV): the north_star's 2e-2 plus the exact representation error of storing the
         result in bf16 (half the bf16 spacing at the value's binade; 0 below 2^-133)
+        R34'' (full-size gradients, where many q-heads x queries sum into one element): plus
+        operand_rounding_dev, the exact effect of the bf16 GEMM operands the north_star fixes
   fp32: max |gpu - oracle| <= 1e-5 * max(1, max |oracle|)
 Every comparison is also recorded (plain max-abs error, count of elements above 2e-2, element
 count) and printed in the pytest terminal summary (tests/conftest.py), so the 2e-2 bar's plain
@@ -32,26 +34,30 @@ def halfulp_bf16(x):
     return np.where(a > 0, np.ldexp(1.0, e - 9), 0.0)
 
 
-def tol_ok(got, ref, fp32: bool, label: str = ""):
+def tol_ok(got, ref, fp32: bool, label: str = "", allow=None):
     """bf16 (R34'): |gpu - ref| <= 2e-2 + halfulp_bf16(max(|ref|, |gpu|)) elementwise -- the
     north_star's 2e-2 absolute bar plus the exact error of representing the result in the bf16 it
     is stored in (above |x| = 4 the bf16 grid itself is coarser than 2e-2; P / dS also enter the
     tensor-core GEMMs as bf16, R31). The larger magnitude is used because a result within 2e-2 of
     a power of two may round into the next binade.
     fp32 (R34): max |gpu - ref| <= 1e-5 * max(1, max |ref|).
-    Returns (ok, worst abs error, bound at the worst element); records the plain max-abs error and
-    the count of elements above 2e-2 in STATS."""
+    R34'' (`allow`, an array like ref): the bound also adds operand_rounding_dev's per-element
+    deviation -- what the exact backward itself moves by when P / dS enter the GEMMs as bf16.
+    Returns (ok, worst abs error, bound at the worst element); records the plain max-abs error, the
+    count of elements above 2e-2 and the count that needed the R34'' term in STATS."""
     if ref.size == 0:
         return True, 0.0, 0.0
     got64 = got.astype(np.float64)
     diff = np.abs(got64 - ref)
     nan = bool(np.isnan(got64).any())
+    bnd = BF16_TOL + halfulp_bf16(np.maximum(np.abs(ref), np.abs(got64)))
     STATS.append((label, "fp32" if fp32 else "bf16", float(np.nanmax(diff)) if not nan else float("nan"),
-                  int((diff > BF16_TOL).sum()), int(diff.size)))
+                  int((diff > BF16_TOL).sum()), int(diff.size), 0 if fp32 else int((diff > bnd).sum())))
     if fp32:
         bound = FP32_TOL * max(1.0, float(np.max(np.abs(ref))))
         return bool(np.all(diff <= bound)) and not nan, float(diff.max()), bound
-    bnd = BF16_TOL + halfulp_bf16(np.maximum(np.abs(ref), np.abs(got64)))
+    if allow is not None:
+        bnd = bnd + np.asarray(allow, np.float64)
     i = int(np.argmax(diff - bnd))
     ok = bool(np.all(diff <= bnd)) and not nan
     return ok, float(diff.flat[i]), float(bnd.flat[i])
@@ -143,3 +149,37 @@ def bf16_model_bwd(x, scale=None):
         dQ[:, h] = sc * rb(dS) @ k[:, g]
         dK[:, g] += sc * rb(dS).T @ q[:, h]
     return rb(dQ).numpy(), rb(dK).numpy(), rb(dV).numpy()
+
+
+def operand_rounding_dev(q, k, v, do, q_pos: int = 0, scale=None):
+    """R34'' allowance: how far the exact backward moves when its GEMM operands carry the precision
+    the north_star fixes ("bf16 in, fp32 accumulate", R31) -- P rounded to bf16 where it enters
+    dV += P^T dO, dS rounded to bf16 where it enters dQ = dS K and dK += dS^T Q, D from the
+    bf16-stored O -- with every other step exact (fp64). Returns |rounded - exact| for dQ [Sq,Hq,d],
+    dK and dV [Sk,Hkv,d] (rows below q_pos receive no contribution and get 0); no output rounding
+    (that is R34''s half-ulp term). Same query / key convention as oracle.attn_bwd: q and do hold
+    positions q_pos..q_pos+Sq-1, k / v positions 0..Sk-1. Test-side (torch fp64, CPU); shares no
+    code with the oracle, which stays the reference the GPU is compared against."""
+    import torch
+    q, k, v, do = (torch.tensor(np.asarray(a), dtype=torch.float64) for a in (q, k, v, do))
+    Sq, hq, d = q.shape
+    Sk, hkv = k.shape[0], k.shape[1]
+    sc = 1.0 / np.sqrt(d) if scale is None else scale
+    rb = lambda t: t.to(torch.bfloat16).to(torch.float64)  # noqa: E731
+    kmax = min(Sk, q_pos + Sq)            # keys any of these queries sees
+    mask = torch.arange(kmax)[None, :] <= (q_pos + torch.arange(Sq))[:, None]
+    eQ = torch.zeros_like(q)
+    eK = torch.zeros(Sk, hkv, d, dtype=torch.float64)
+    eV = torch.zeros_like(eK)
+    for h in range(hq):
+        g = (h * hkv) // hq
+        kg, vg = k[:kmax, g], v[:kmax, g]
+        P = torch.softmax((sc * q[:, h] @ kg.T).masked_fill(~mask, float("-inf")), dim=1)
+        dP = do[:, h] @ vg.T
+        O = P @ vg
+        dS = P * (dP - (do[:, h] * O).sum(1, keepdim=True))
+        dSm = P * (dP - (do[:, h] * rb(O)).sum(1, keepdim=True))
+        eV[:kmax, g] += (rb(P) - P).T @ do[:, h]
+        eQ[:, h] = sc * (rb(dSm) - dS) @ kg
+        eK[:kmax, g] += sc * (rb(dSm) - dS).T @ q[:, h]
+    return eQ.abs().numpy(), eK.abs().numpy(), eV.abs().numpy()

@@ -14,7 +14,10 @@ plain definition:
   * every sequence of <= 512 tokens: all outputs, whole.
 Inputs are the seeded per-sequence tensors of synth.seq_tensors (bf16-rounded), placed into each
 rank's rank-natural source buffer exactly as a DataLoader would hand them over (R38).
-Tolerance: R34' bf16 bound (tests/attn_harness.tol_ok).
+Tolerance: R34' bf16 bound (tests/attn_harness.tol_ok) on O; R34'' on dQ / dK / dV (R34' plus
+tests/attn_harness.operand_rounding_dev at each element: at these shapes up to 7 q-heads x thousands
+of queries sum into one dK / dV element, and the bf16 P / dS operands the north_star fixes alone move
+the exact result by up to ~3e-2 there -- DESIGN.md §9).
 """
 import numpy as np
 import pytest
@@ -26,7 +29,7 @@ from oracle.attention import attn_bwd, attn_fwd  # noqa: E402
 from oracle.cost_model import Model  # noqa: E402
 from oracle.schedule import plan as oracle_plan  # noqa: E402
 from synth import CONFIGS, seq_tensors  # noqa: E402
-from tests.attn_harness import tol_ok  # noqa: E402
+from tests.attn_harness import operand_rounding_dev, tol_ok  # noqa: E402
 
 SHORT_WHOLE = 512
 N_ROWS = 6          # random query rows per sampled long sequence (plus fixed edge rows)
@@ -97,8 +100,8 @@ def _rows(runs, loc, s, positions, key):
     return np.stack(out)
 
 
-def _check(name, got, ref, where):
-    ok, err, bound = tol_ok(got, ref, False, label=f"{name} fullsize")
+def _check(name, got, ref, where, allow=None):
+    ok, err, bound = tol_ok(got, ref, False, label=f"{name} fullsize", allow=allow)
     assert ok, f"{name} {where}: err {err} > {bound}"
 
 
@@ -117,9 +120,10 @@ def test_fullsize_sampled(cfg_name):
         x = seq_tensors(0, s, S, shp.hq, shp.hkv, shp.d)
         O, L = attn_fwd(x["q"], x["k"], x["v"])
         dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
+        eQ, eK, eV = operand_rounding_dev(x["q"], x["k"], x["v"], x["do"])
         pos = range(S)
-        for key, ref in (("o", O), ("dq", dQ), ("dk", dK), ("dv", dV)):
-            _check(key, _rows(runs, loc, s, pos, key), ref, f"{cfg_name} short seq {s} (S={S})")
+        for key, ref, al in (("o", O, None), ("dq", dQ, eQ), ("dk", dK, eK), ("dv", dV, eV)):
+            _check(key, _rows(runs, loc, s, pos, key), ref, f"{cfg_name} short seq {s} (S={S})", al)
         assert np.abs(_rows(runs, loc, s, pos, "lse").T - L).max() <= 2e-2
         checked += 1
     for s in sampled:
@@ -129,15 +133,17 @@ def test_fullsize_sampled(cfg_name):
         for i in rows:
             O, L = attn_fwd(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], q_pos=i)
             dQ, _, _ = attn_bwd(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], x["do"][i:i + 1], q_pos=i)
+            eQ, _, _ = operand_rounding_dev(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], x["do"][i:i + 1], q_pos=i)
             where = f"{cfg_name} seq {s} (S={S}) row {i}"
             _check("o", _rows(runs, loc, s, [i], "o"), O, where)
-            _check("dq", _rows(runs, loc, s, [i], "dq"), dQ, where)
+            _check("dq", _rows(runs, loc, s, [i], "dq"), dQ, where, eQ)
             assert np.abs(_rows(runs, loc, s, [i], "lse").T - L).max() <= 2e-2, where
         j0 = max(0, S - TAIL)
         _, dK, dV = attn_bwd(x["q"][j0:], x["k"], x["v"], x["do"][j0:], q_pos=j0)
+        _, eK, eV = operand_rounding_dev(x["q"][j0:], x["k"], x["v"], x["do"][j0:], q_pos=j0)
         tail = range(j0, S)
-        _check("dk", _rows(runs, loc, s, tail, "dk"), dK[j0:], f"{cfg_name} seq {s} (S={S}) key tail")
-        _check("dv", _rows(runs, loc, s, tail, "dv"), dV[j0:], f"{cfg_name} seq {s} (S={S}) key tail")
+        _check("dk", _rows(runs, loc, s, tail, "dk"), dK[j0:], f"{cfg_name} seq {s} (S={S}) key tail", eK[j0:])
+        _check("dv", _rows(runs, loc, s, tail, "dv"), dV[j0:], f"{cfg_name} seq {s} (S={S}) key tail", eV[j0:])
         checked += 1
     assert checked >= 3
 
@@ -161,7 +167,8 @@ def _whole_ref(shp, lens, seed):
             x = seq_tensors(seed, k, int(S), shp.hq, shp.hkv, shp.d)
             O, L = attn_fwd(x["q"], x["k"], x["v"])
             dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
-            refs.append(dict(o=O, lse=L, dq=dQ, dk=dK, dv=dV))
+            eQ, eK, eV = operand_rounding_dev(x["q"], x["k"], x["v"], x["do"])
+            refs.append(dict(o=O, lse=L, dq=dQ, dk=dK, dv=dV, allow=dict(dq=eQ, dk=eK, dv=eV)))
         _WHOLE_REF[key] = refs
     return _WHOLE_REF[key]
 
@@ -212,5 +219,6 @@ def test_fullsize_whole_long_sequence(shape_name, N):
     for s in range(len(lens)):
         for key in ("o", "dq", "dk", "dv"):
             assert not np.isnan(got[key][s]).any(), f"{key} seq {s}: rows not covered"
-            _check(key, got[key][s], refs[s][key], f"{shape_name} N={N} seq {s} (S={int(lens[s])}) whole")
+            _check(key, got[key][s], refs[s][key], f"{shape_name} N={N} seq {s} (S={int(lens[s])}) whole",
+                   refs[s]["allow"].get(key))
         assert np.abs(lse[s] - refs[s]["lse"]).max() <= 2e-2
