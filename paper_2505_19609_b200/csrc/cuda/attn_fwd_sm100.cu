@@ -118,7 +118,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define SKR_FWD_ROWSPLIT 1
 #endif
 #ifndef SKR_FWD_PVFIRST
-#define SKR_FWD_PVFIRST 0
+#define SKR_FWD_PVFIRST 1   // MMA thread: PV_A(j-1) before the K(j) wait (S4n1 fwd -2 %, r02_run31)
 #endif
 
 template <int D>
