@@ -2,7 +2,7 @@
 plan, RankStep tables and C-ABI calls), on outputs the fp64 oracle can compute one by one.
 
 BASELINE configs[1..4] at full size: C2, C3n2 (configs[2]), C4 (configs[3], CP=8 loopback), C5n1
-(configs[4] at N=1). Full batches are far beyond what the naive oracle finishes in seconds (C2's
+(configs[4] at N=1); C3n2 also through the ring exchange (row f4) and the fused peer exchange (row f3). Full batches are far beyond what the naive oracle finishes in seconds (C2's
 32K sequence alone is ~1e12 fp64 flop), so each check is on a SAMPLE whose oracle values are exact
 restrictions of the
 plain definition:
@@ -36,10 +36,14 @@ N_ROWS = 6          # random query rows per sampled long sequence (plus fixed ed
 TAIL = 192          # key rows checked at the end of each sampled long sequence
 
 
-def _launch(cfg_name, seed):
-    """Plan + run one fwd+bwd step of the whole batch as bench.py does; returns per-seq lookups."""
+def _launch(cfg_name, seed, exchange="nccl"):
+    """Plan + run one fwd+bwd step of the whole batch as bench.py does; returns per-seq lookups.
+    exchange: the CP exchange the loopback emulates -- "nccl" (all-gather / reduce-scatter, the
+    default), "ring" (row f4's alternative) or "fused" (row f3: peer gather, dK/dV red-added into the
+    owners' accumulators from the backward epilogue)."""
     from paper_2505_19609_b200 import skrull as sk
-    from paper_2505_19609_b200.runtime import RankStep, loopback_step, rank_natural_rows
+    from paper_2505_19609_b200.runtime import (RankStep, loopback_peer_fused_step, loopback_ring_step,
+                                               loopback_step, rank_natural_rows)
     cfg = CONFIGS[cfg_name]
     lens = cfg.lengths(seed)
     shp, N, C = cfg.shape, cfg.cp, cfg.bucket
@@ -58,7 +62,7 @@ def _launch(cfg_name, seed):
     for j in range(int(p["n_mb_per_dp"][0])):
         idx = np.nonzero(p["mb_of_seq"] == j)[0]
         ml, ma = lens[idx], p["assign"][idx]
-        ranks = [RankStep(shape, ml, ma, N, r) for r in range(N)]
+        ranks = [RankStep(shape, ml, ma, N, r, ring=exchange == "ring") for r in range(N)]
         srcs = {}
         for name in ("q", "k", "v", "do"):
             srcs[name] = []
@@ -71,7 +75,8 @@ def _launch(cfg_name, seed):
             ranks[0].forward(srcs["q"][0], srcs["k"][0], srcs["v"][0], None, side)
             ranks[0].backward(srcs["do"][0], None, side)
         else:
-            loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+            step = {"ring": loopback_ring_step, "fused": loopback_peer_fused_step}.get(exchange, loopback_step)
+            step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
         torch.cuda.synchronize()
         for r, rs in enumerate(ranks):
             pr = rs.pr
@@ -105,9 +110,10 @@ def _check(name, got, ref, where, allow=None):
     assert ok, f"{name} {where}: err {err} > {bound}"
 
 
-@pytest.mark.parametrize("cfg_name", ["C2", "C5n1", "C3n2", "C4"])
-def test_fullsize_sampled(cfg_name):
-    cfg, lens, runs, loc = _launch(cfg_name, 0)
+@pytest.mark.parametrize("cfg_name,exchange", [("C2", "nccl"), ("C5n1", "nccl"), ("C3n2", "nccl"), ("C4", "nccl"),
+                                               ("C3n2", "ring"), ("C3n2", "fused")])
+def test_fullsize_sampled(cfg_name, exchange):
+    cfg, lens, runs, loc = _launch(cfg_name, 0, exchange)
     rng = np.random.default_rng(1234)
     order = np.argsort(lens, kind="stable")
     longest = int(order[-1])
@@ -173,11 +179,12 @@ def _whole_ref(shp, lens, seed):
     return _WHOLE_REF[key]
 
 
-@pytest.mark.parametrize("N", [1, 8])
-@pytest.mark.parametrize("shape_name", ["qwen05", "qwen7"])
-def test_fullsize_whole_long_sequence(shape_name, N):
+@pytest.mark.parametrize("shape_name,N,exchange", [("qwen05", 1, "nccl"), ("qwen05", 8, "nccl"), ("qwen7", 1, "nccl"),
+                                                   ("qwen7", 8, "nccl"), ("qwen7", 8, "ring"), ("qwen7", 8, "fused")])
+def test_fullsize_whole_long_sequence(shape_name, N, exchange):
     from paper_2505_19609_b200 import skrull as sk
-    from paper_2505_19609_b200.runtime import RankStep, gather_rank_natural, loopback_step
+    from paper_2505_19609_b200.runtime import (RankStep, gather_rank_natural, loopback_peer_fused_step,
+                                               loopback_ring_step, loopback_step)
     from synth.configs import QWEN05, QWEN7
     shp = {"qwen05": QWEN05, "qwen7": QWEN7}[shape_name]
     seed = 11
@@ -191,7 +198,7 @@ def test_fullsize_whole_long_sequence(shape_name, N):
     assert (p["assign"][0] == -1) == (N > 1)
     shape = sk.attn_shape(shp.hq, shp.hkv, shp.d, sk.SKR_BF16)
     inputs = [seq_tensors(seed, k, int(S), shp.hq, shp.hkv, shp.d) for k, S in enumerate(lens)]
-    ranks = [RankStep(shape, lens, p["assign"], N, r) for r in range(N)]
+    ranks = [RankStep(shape, lens, p["assign"], N, r, ring=exchange == "ring") for r in range(N)]
     srcs = {k: [torch.from_numpy(gather_rank_natural(inputs, lens, p["assign"], N, r, k)).to("cuda", torch.bfloat16)
                 for r in range(N)] for k in ("q", "k", "v", "do")}
     if N == 1:
@@ -199,7 +206,8 @@ def test_fullsize_whole_long_sequence(shape_name, N):
         ranks[0].forward(srcs["q"][0], srcs["k"][0], srcs["v"][0], None, side)
         ranks[0].backward(srcs["do"][0], None, side)
     else:
-        loopback_step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
+        step = {"ring": loopback_ring_step, "fused": loopback_peer_fused_step}.get(exchange, loopback_step)
+        step(ranks, srcs["q"], srcs["k"], srcs["v"], srcs["do"])
     torch.cuda.synchronize()
     got = {key: [np.full((int(S),) + inputs[k]["q" if key in ("o", "dq") else "k"].shape[1:], np.nan)
                  for k, S in enumerate(lens)] for key in ("o", "dq", "dk", "dv")}
@@ -219,6 +227,6 @@ def test_fullsize_whole_long_sequence(shape_name, N):
     for s in range(len(lens)):
         for key in ("o", "dq", "dk", "dv"):
             assert not np.isnan(got[key][s]).any(), f"{key} seq {s}: rows not covered"
-            _check(key, got[key][s], refs[s][key], f"{shape_name} N={N} seq {s} (S={int(lens[s])}) whole",
+            _check(key, got[key][s], refs[s][key], f"{shape_name} N={N} {exchange} seq {s} (S={int(lens[s])}) whole",
                    refs[s]["allow"].get(key))
         assert np.abs(lse[s] - refs[s]["lse"]).max() <= 2e-2
