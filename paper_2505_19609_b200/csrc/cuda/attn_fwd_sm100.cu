@@ -426,7 +426,10 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
               pa.mark(2);
             }
 #if SKR_FWD_PVFIRST
-            if (s == 0 && j < n_kv) wait_k(j);   // PV_A(j-1) needs only V(j-1): issue it before K(j) lands
+            if (s == 0 && j < n_kv) {   // PV_A(j-1) needs only V(j-1): issue it before K(j) lands
+              wait_k(j);
+              tc_fence_after();
+            }
 #endif
             if (j < n_kv) issue_s(s, kunit(j, s));
             trace(3 + s, jv);
