@@ -117,6 +117,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef SKR_FWD_ROWSPLIT
 #define SKR_FWD_ROWSPLIT 1
 #endif
+#ifndef SKR_FWD_ORDER64
+#define SKR_FWD_ORDER64 0
+#endif
 #ifndef SKR_FWD_PVFIRST
 #define SKR_FWD_PVFIRST 1   // MMA thread: PV_A(j-1) before the K(j) wait (S4n1 fwd -2 %, r02_run31)
 #endif
@@ -366,7 +369,28 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
       auto free_v = [&](int j) {
         for (int t = 0; t < nstream; ++t) umma_commit(&bars->kv_empty[vunit(j, t)]);
       };
-      if (!C::kPAlias) {
+      if (!C::kPAlias && SKR_FWD_ORDER64 && kWG == 2) {
+        // experiment (SKR_FWD_ORDER64): per head [S_s(j), PV_s(j-1)] instead of [S_A S_B][PV_A PV_B],
+        // so head A's PV(j-1) never waits behind head B's s_free
+        for (int j = 0; j <= n_kv; ++j) {
+          if (j < n_kv) wait_k(j);
+          if (j > 0) wait_v(j - 1);
+          for (int s = 0; s < nq; ++s) {
+            if (j < n_kv) {
+              if (j > 0) mbar_wait(&bars->s_free[s], (j - 1) & 1);
+              tc_fence_after();
+              issue_s(s, kunit(j, s));
+            }
+            if (j > 0) {
+              mbar_wait(&bars->p_full[s], (j - 1) & 1);
+              tc_fence_after();
+              issue_pv(s, vunit(j - 1, s), j - 1 > 0);
+            }
+          }
+          if (j < n_kv) free_k(j);
+          if (j > 0) free_v(j - 1);
+        }
+      } else if (!C::kPAlias) {
         for (int j = 0; j <= n_kv; ++j) {
           if (j < n_kv) {
             wait_k(j);
