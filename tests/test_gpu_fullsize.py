@@ -105,6 +105,20 @@ def _rows(runs, loc, s, positions, key):
     return np.stack(out)
 
 
+def _lazy(fn, *args, **kw):
+    """R34'' allowance computed at most once and only on demand: _lazy(f, ...)(i) is a callable
+    returning f(...)[i] (tol_ok evaluates it only when some element exceeds R34')."""
+    memo = []
+
+    def part(i):
+        def get():
+            if not memo:
+                memo.append(fn(*args, **kw))
+            return memo[0][i]
+        return get
+    return part
+
+
 def _check(name, got, ref, where, allow=None):
     ok, err, bound = tol_ok(got, ref, False, label=f"{name} fullsize", allow=allow)
     assert ok, f"{name} {where}: err {err} > {bound}"
@@ -126,9 +140,9 @@ def test_fullsize_sampled(cfg_name, exchange):
         x = seq_tensors(0, s, S, shp.hq, shp.hkv, shp.d)
         O, L = attn_fwd(x["q"], x["k"], x["v"])
         dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
-        eQ, eK, eV = operand_rounding_dev(x["q"], x["k"], x["v"], x["do"])
+        dev = _lazy(operand_rounding_dev, x["q"], x["k"], x["v"], x["do"])
         pos = range(S)
-        for key, ref, al in (("o", O, None), ("dq", dQ, eQ), ("dk", dK, eK), ("dv", dV, eV)):
+        for key, ref, al in (("o", O, None), ("dq", dQ, dev(0)), ("dk", dK, dev(1)), ("dv", dV, dev(2))):
             _check(key, _rows(runs, loc, s, pos, key), ref, f"{cfg_name} short seq {s} (S={S})", al)
         assert np.abs(_rows(runs, loc, s, pos, "lse").T - L).max() <= 2e-2
         checked += 1
@@ -139,17 +153,20 @@ def test_fullsize_sampled(cfg_name, exchange):
         for i in rows:
             O, L = attn_fwd(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], q_pos=i)
             dQ, _, _ = attn_bwd(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], x["do"][i:i + 1], q_pos=i)
-            eQ, _, _ = operand_rounding_dev(x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], x["do"][i:i + 1], q_pos=i)
+            dev = _lazy(operand_rounding_dev, x["q"][i:i + 1], x["k"][:i + 1], x["v"][:i + 1], x["do"][i:i + 1],
+                        q_pos=i)
             where = f"{cfg_name} seq {s} (S={S}) row {i}"
             _check("o", _rows(runs, loc, s, [i], "o"), O, where)
-            _check("dq", _rows(runs, loc, s, [i], "dq"), dQ, where, eQ)
+            _check("dq", _rows(runs, loc, s, [i], "dq"), dQ, where, dev(0))
             assert np.abs(_rows(runs, loc, s, [i], "lse").T - L).max() <= 2e-2, where
         j0 = max(0, S - TAIL)
         _, dK, dV = attn_bwd(x["q"][j0:], x["k"], x["v"], x["do"][j0:], q_pos=j0)
-        _, eK, eV = operand_rounding_dev(x["q"][j0:], x["k"], x["v"], x["do"][j0:], q_pos=j0)
+        dev = _lazy(operand_rounding_dev, x["q"][j0:], x["k"], x["v"], x["do"][j0:], q_pos=j0)
         tail = range(j0, S)
-        _check("dk", _rows(runs, loc, s, tail, "dk"), dK[j0:], f"{cfg_name} seq {s} (S={S}) key tail", eK[j0:])
-        _check("dv", _rows(runs, loc, s, tail, "dv"), dV[j0:], f"{cfg_name} seq {s} (S={S}) key tail", eV[j0:])
+        _check("dk", _rows(runs, loc, s, tail, "dk"), dK[j0:], f"{cfg_name} seq {s} (S={S}) key tail",
+               lambda: dev(1)()[j0:])
+        _check("dv", _rows(runs, loc, s, tail, "dv"), dV[j0:], f"{cfg_name} seq {s} (S={S}) key tail",
+               lambda: dev(2)()[j0:])
         checked += 1
     assert checked >= 3
 
@@ -173,8 +190,8 @@ def _whole_ref(shp, lens, seed):
             x = seq_tensors(seed, k, int(S), shp.hq, shp.hkv, shp.d)
             O, L = attn_fwd(x["q"], x["k"], x["v"])
             dQ, dK, dV = attn_bwd(x["q"], x["k"], x["v"], x["do"])
-            eQ, eK, eV = operand_rounding_dev(x["q"], x["k"], x["v"], x["do"])
-            refs.append(dict(o=O, lse=L, dq=dQ, dk=dK, dv=dV, allow=dict(dq=eQ, dk=eK, dv=eV)))
+            dev = _lazy(operand_rounding_dev, x["q"], x["k"], x["v"], x["do"])
+            refs.append(dict(o=O, lse=L, dq=dQ, dk=dK, dv=dV, allow=dict(dq=dev(0), dk=dev(1), dv=dev(2))))
         _WHOLE_REF[key] = refs
     return _WHOLE_REF[key]
 

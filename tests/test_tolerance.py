@@ -69,4 +69,9 @@ def test_tol_ok_allowance_is_additive():
     assert not tol_ok(got, ref, False)[0]
     assert tol_ok(got, ref, False, allow=np.array([0.002, 0.0]))[0]
     assert not tol_ok(got, ref, False, allow=np.array([0.0005, 0.0]))[0]
+    # a callable allowance is evaluated only when some element exceeds R34'
+    calls = []
+    allow = lambda: calls.append(1) or np.array([0.002, 0.0])  # noqa: E731
+    assert tol_ok(ref + np.array([0.01, 0.0]), ref, False, allow=allow)[0] and not calls
+    assert tol_ok(got, ref, False, allow=allow)[0] and len(calls) == 1
     del attn_harness.STATS[n0:]
