@@ -117,6 +117,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef SKR_FWD_ROWSPLIT
 #define SKR_FWD_ROWSPLIT 1
 #endif
+// SKR_FWD_SSPLIT (experiment, d = 128 row split): P goes to the SECOND half of S's columns and
+// S(j+1) is issued as two N = 64 halves -- the first (keys [0, 64), columns [0, 64)) as soon as the
+// softmax has loaded S(j), the second after PV(j) -- so only PV + half an S stay on each head's chain.
+#ifndef SKR_FWD_SSPLIT
+#define SKR_FWD_SSPLIT 0
+#endif
 #ifndef SKR_FWD_ORDER64
 #define SKR_FWD_ORDER64 0
 #endif
@@ -150,7 +156,9 @@ struct Cfg {
   static constexpr bool kPAlias = D == 128 && BN == 128;
   __device__ static constexpr uint32_t tS(int s) { return s * BN; }
   __device__ static constexpr uint32_t tO(int s) { return 256 + s * D; }
-  __device__ static constexpr uint32_t tP(int s) { return kPAlias ? s * 128 : (D == 128 ? 128 + s * 32 : 384 + s * 64); }
+  __device__ static constexpr uint32_t tP(int s) {
+    return kPAlias ? s * 128 + (SKR_FWD_SSPLIT ? 64 : 0) : (D == 128 ? 128 + s * 32 : 384 + s * 64);
+  }
 };
 
 struct Bars {  // kUnits <= 8
@@ -308,6 +316,18 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         }
         umma_commit(&bars->s_full[s]);
       };
+      // SKR_FWD_SSPLIT: one N = 64 half of S (keys / columns [64 h, 64 h + 64)); the caller commits
+      const uint32_t id_s64 = idesc_bf16_f32(BM, 64, 0, 0);
+      auto issue_s_half = [&](int s, int u, int h) {
+        const uint64_t dq = dq0 + ((uint32_t)(s * C::kQBytes) >> 4);
+        const uint64_t dk = dkv0 + ((uint32_t)(u * C::kKVBytes + h * 64 * 128) >> 4);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = ((k / 4) * (BM * 128) + (k % 4) * 32) >> 4;
+          const uint32_t koff = ((k / 4) * (BN * 128) + (k % 4) * 32) >> 4;
+          umma_f16(tmem + C::tS(s) + 64 * h, dq + off, dk + koff, id_s64, k > 0);
+        }
+      };
       // Row split with P aliasing S: the softmax never waits for an intermediate PV (s_full(j) implies
       // PV(j-1)), so pv_done is committed once, after the last PV (an arrive nobody waits for is what
       // compute-sanitizer's synccheck reports); its epilogue waits for phase 0
@@ -424,6 +444,35 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
             }
             free_v(jv);
           }
+        }
+      } else if (SKR_FWD_SSPLIT && kWG == 2 && kRowSplit) {
+        wait_k(0);
+        tc_fence_after();
+        for (int s = 0; s < nq; ++s) issue_s(s, kunit(0, s));
+        free_k(0);
+        for (int j = 1; j <= n_kv; ++j) {
+          const int jv = j - 1;
+          wait_v(jv);
+          if (j < n_kv) {
+            wait_k(j);
+            tc_fence_after();
+          }
+          for (int s = 0; s < nq; ++s) {
+            if (j < n_kv) {   // the softmax has S_s(j-1) in registers: keys [0, 64) of S_s(j) may go in
+              mbar_wait(&bars->p_lo[s], jv & 1);
+              tc_fence_after();
+              issue_s_half(s, kunit(j, s), 0);
+            }
+            mbar_wait(&bars->p_full[s], jv & 1);
+            tc_fence_after();
+            issue_pv(s, vunit(jv, s), jv > 0, j == n_kv);
+            if (j < n_kv) {
+              issue_s_half(s, kunit(j, s), 1);
+              umma_commit(&bars->s_full[s]);
+            }
+          }
+          free_v(jv);
+          if (j < n_kv) free_k(j);
         }
       } else {
         wait_k(0);
@@ -695,6 +744,9 @@ __global__ void __launch_bounds__((8 * kWG + 2) * 32, 1)
         if (!C::kPAlias) {
           tc_fence_before();
           mbar_arrive(&bars->s_free[s]);      // S_s TMEM may now take S_s(j+1)
+        } else if (SKR_FWD_SSPLIT && j + 1 < n_kv) {
+          tc_fence_before();
+          mbar_arrive(&bars->p_lo[s]);        // columns [0, 64) may take keys [0, 64) of S_s(j+1)
         }
         const int kv0 = j * BN;
         if (kv0 + BN - 1 > qp0 || kv0 + BN > k_len) {   // diagonal / last tile: mask keys after the query

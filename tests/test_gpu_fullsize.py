@@ -196,8 +196,9 @@ def _whole_ref(shp, lens, seed):
     return _WHOLE_REF[key]
 
 
-@pytest.mark.parametrize("shape_name,N,exchange", [("qwen05", 1, "nccl"), ("qwen05", 8, "nccl"), ("qwen7", 1, "nccl"),
-                                                   ("qwen7", 8, "nccl"), ("qwen7", 8, "ring"), ("qwen7", 8, "fused")])
+@pytest.mark.parametrize("shape_name,N,exchange", [("qwen05", 1, "nccl"), ("qwen05", 8, "nccl"), ("qwen05", 8, "ring"),
+                                                   ("qwen05", 8, "fused"), ("qwen7", 1, "nccl"), ("qwen7", 8, "nccl"),
+                                                   ("qwen7", 8, "ring"), ("qwen7", 8, "fused")])
 def test_fullsize_whole_long_sequence(shape_name, N, exchange):
     from paper_2505_19609_b200 import skrull as sk
     from paper_2505_19609_b200.runtime import (RankStep, gather_rank_natural, loopback_peer_fused_step,
